@@ -405,7 +405,7 @@ def train_fes(Xr: torch.Tensor, flags: np.ndarray, r: int, n_e: int, seed: int,
 # brute force in tests/test_datagen.py)
 # ----------------------------------------------------------------------------
 def ground_truth(Qh: torch.Tensor, Xh: torch.Tensor, k: int, metric: str = "l2",
-                 ids: Optional[torch.Tensor] = None, slack: int = 32, chunk: int = 1 << 20):
+                 ids: Optional[torch.Tensor] = None, slack: int = 32, chunk: Optional[int] = None):
     """Exact top-k by (δ, id) of each query row of Qh (fp64) over rows `ids` of
     Xh (fp32): fp32 scan keeps k+slack candidates, then an fp64 direct-form
     re-rank with ties to the smaller id.  → (ids int64 [m][k], δ fp64 [m][k])."""
@@ -414,6 +414,8 @@ def ground_truth(Qh: torch.Tensor, Xh: torch.Tensor, k: int, metric: str = "l2",
     if ids is None:
         ids = torch.arange(Xh.shape[0], device=dev)
     kk = min(k + slack, ids.numel())
+    if chunk is None:                       # keep the m × chunk score block ≲ 1.5 GB
+        chunk = int(min(1 << 20, max(4096, 1.5e9 // (4 * max(1, m)))))
     best_v = torch.full((m, kk), float("inf"), device=dev)
     best_i = torch.full((m, kk), -1, dtype=torch.int64, device=dev)
     Qf = Qh.float().to(dev)

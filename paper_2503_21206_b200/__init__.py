@@ -1,0 +1,255 @@
+"""Python binding of the B200-native PilotANN GPU stage (arXiv 2503.21206).
+
+Argument marshalling only: every step of the search runs in the CUDA kernels /
+C++ runtime of libpilotann.so behind include/pilotann.h.  There is no Python
+or CPU fallback for the GPU stage: if the shared library is missing, importing
+works (so the package can be inspected / built) but constructing an Index
+raises immediately.
+
+    import paper_2503_21206_b200 as pa
+    ix = pa.Index(n=..., dim=..., rdim=..., sub_offsets=..., ...)   # pa_build
+    ix.attach_host(full_offsets, full_neighbors, rotated)             # pa_attach_host (stages 2-3)
+    ids, d = ix.search(queries, k=10, ef=64)                          # pa_search (host buffers)
+    ix.search_device(q_dev, k, ef, out_ids_dev, out_d_dev)            # pa_search_device (torch tensors)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpilotann.so")
+
+PA_OK, PA_EINVAL, PA_EGRAPH, PA_EBASIS, PA_EFES, PA_ENOMEM, PA_ECUDA, PA_ESTATE, PA_ENOTSUP = 0, -1, -2, -3, -4, -5, -6, -7, -8
+STATUS_NAMES = {0: "PA_OK", -1: "PA_EINVAL", -2: "PA_EGRAPH", -3: "PA_EBASIS", -4: "PA_EFES",
+                -5: "PA_ENOMEM", -6: "PA_ECUDA", -7: "PA_ESTATE", -8: "PA_ENOTSUP"}
+PA_L2, PA_IP = 0, 1
+PA_STAGES_GPU, PA_STAGES_FULL = 1, 3
+PA_NO_FES, PA_NO_STAGE2, PA_NO_STAGE1 = 1, 2, 4
+
+# Symbols declared in include/pilotann.h (checked by tests/test_abi.py).
+EXPORTS = ("pa_build", "pa_attach_host", "pa_search", "pa_search_device", "pa_search_candidates",
+           "pa_get_stats", "pa_destroy", "pa_last_error", "pa_version")
+
+
+class PAError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class BuildParams(C.Structure):
+    _fields_ = [("n", C.c_int64), ("dim", C.c_int32), ("rdim", C.c_int32), ("max_degree", C.c_int32),
+                ("metric", C.c_int32), ("sub_offsets", C.c_void_p), ("sub_neighbors", C.c_void_p),
+                ("member_flags", C.c_void_p), ("reduced", C.c_void_p), ("basis", C.c_void_p),
+                ("fes_r", C.c_int32), ("fes_centroids", C.c_void_p), ("fes_cell_off", C.c_void_p),
+                ("fes_pool_ids", C.c_void_p), ("device", C.c_int32)]
+
+
+class SearchOpts(C.Structure):
+    _fields_ = [("stages", C.c_int32), ("ef1", C.c_int32), ("ef2", C.c_int32), ("ef3", C.c_int32),
+                ("entries", C.c_int32), ("width", C.c_int32), ("refine_iters", C.c_int32),
+                ("flags", C.c_uint32), ("hash_slots_log2", C.c_int32), ("host_threads", C.c_int32)]
+
+
+class Debug(C.Structure):
+    _fields_ = [("cell", C.c_void_p), ("entries", C.c_void_p), ("cand_ids", C.c_void_p),
+                ("cand_dists", C.c_void_p), ("counters", C.c_void_p), ("trace_cap", C.c_int32),
+                ("trace_expand", C.c_void_p), ("trace_visit", C.c_void_p), ("trace_nexp", C.c_void_p),
+                ("trace_nvis", C.c_void_p)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("queries", C.c_int64), ("kernel_launches", C.c_int64),
+                ("ms_project", C.c_double), ("ms_fes", C.c_double), ("ms_traverse", C.c_double),
+                ("ms_total_gpu", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double),
+                ("ms_host_stages", C.c_double), ("ms_wall", C.c_double),
+                ("sum_n_exp", C.c_int64), ("sum_n_dist", C.c_int64), ("sum_spill", C.c_int64),
+                ("overflow_queries", C.c_int64), ("sum_n_dist2", C.c_int64), ("sum_n_dist3", C.c_int64)]
+
+    def asdict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libpilotann.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback for the GPU stage)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.pa_build.restype = C.c_int
+        L.pa_build.argtypes = [C.POINTER(BuildParams), C.POINTER(vp)]
+        L.pa_attach_host.restype = C.c_int
+        L.pa_attach_host.argtypes = [vp, vp, vp, vp]
+        L.pa_search.restype = C.c_int
+        L.pa_search.argtypes = [vp, vp, i64, i32, i32, C.POINTER(SearchOpts), vp, vp]
+        L.pa_search_device.restype = C.c_int
+        L.pa_search_device.argtypes = [vp, vp, i64, i32, i32, C.POINTER(SearchOpts), vp, vp, C.POINTER(Debug), vp]
+        L.pa_search_candidates.restype = C.c_int
+        L.pa_search_candidates.argtypes = [vp, vp, i64, i32, C.POINTER(SearchOpts), vp, vp]
+        L.pa_get_stats.restype = C.c_int
+        L.pa_get_stats.argtypes = [vp, C.POINTER(Stats), C.c_size_t]
+        L.pa_destroy.restype = None
+        L.pa_destroy.argtypes = [vp]
+        L.pa_last_error.restype = C.c_char_p
+        L.pa_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def version() -> str:
+    return lib().pa_version().decode()
+
+
+def _check(rc):
+    if rc != PA_OK:
+        raise PAError(rc, lib().pa_last_error().decode())
+
+
+def _c(a, dt):
+    return None if a is None else np.ascontiguousarray(a, dtype=dt)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def make_opts(stages=PA_STAGES_GPU, ef1=0, ef2=0, ef3=0, entries=0, width=0, refine_iters=0, flags=0,
+              hash_slots_log2=0, host_threads=0) -> SearchOpts:
+    return SearchOpts(stages=stages, ef1=ef1, ef2=ef2, ef3=ef3, entries=entries, width=width,
+                      refine_iters=refine_iters, flags=flags, hash_slots_log2=hash_slots_log2,
+                      host_threads=host_threads)
+
+
+class Index:
+    """One device replica (pa_build).  Arrays are host numpy arrays (copied)."""
+
+    def __init__(self, *, sub_offsets, sub_neighbors, reduced, basis, fes_centroids, fes_cell_off,
+                 fes_pool_ids, member_flags=None, metric="l2", max_degree=None, device=0, n=None):
+        so = _c(sub_offsets, np.int64)
+        sn = _c(sub_neighbors, np.int32)
+        red = _c(reduced, np.float32)
+        bas = _c(basis, np.float32)
+        cen = _c(fes_centroids, np.float32)
+        coff = _c(fes_cell_off, np.int64)
+        pool = _c(fes_pool_ids, np.int32)
+        mf = _c(member_flags, np.uint8)
+        n = int(so.shape[0] - 1) if n is None else int(n)
+        if max_degree is None:
+            max_degree = int(np.diff(so).max()) if so.shape[0] > 1 else 1
+            max_degree = max(1, max_degree)
+        p = BuildParams(n=n, dim=int(bas.shape[0]), rdim=int(red.shape[1]), max_degree=int(max_degree),
+                        metric=PA_IP if metric in ("ip", PA_IP) else PA_L2,
+                        sub_offsets=_ptr(so), sub_neighbors=_ptr(sn), member_flags=_ptr(mf),
+                        reduced=_ptr(red), basis=_ptr(bas), fes_r=int(coff.shape[0] - 1),
+                        fes_centroids=_ptr(cen), fes_cell_off=_ptr(coff), fes_pool_ids=_ptr(pool),
+                        device=int(device))
+        h = C.c_void_p()
+        _check(lib().pa_build(C.byref(p), C.byref(h)))
+        self._h = h
+        self.n, self.dim, self.rdim, self.device = n, p.dim, p.rdim, int(device)
+        self.metric = "ip" if p.metric == PA_IP else "l2"
+        self._host_keep = None
+
+    @classmethod
+    def from_instance(cls, inst: dict, device=0, max_degree=None):
+        return cls(sub_offsets=inst["sub_offsets"], sub_neighbors=inst["sub_neighbors"],
+                   reduced=inst["reduced"], basis=inst["basis"], fes_centroids=inst["fes_centroids"],
+                   fes_cell_off=inst["fes_cell_off"], fes_pool_ids=inst["fes_pool_ids"],
+                   member_flags=inst.get("member_flags"), metric=inst.get("metric", "l2"),
+                   max_degree=max_degree, device=device)
+
+    # -- pa_attach_host -----------------------------------------------------
+    def attach_host(self, full_offsets, full_neighbors, rotated):
+        keep = (_c(full_offsets, np.int64), _c(full_neighbors, np.int32), _c(rotated, np.float32))
+        _check(lib().pa_attach_host(self._h, _ptr(keep[0]), _ptr(keep[1]), _ptr(keep[2])))
+        self._host_keep = keep          # borrowed by the library until destroy
+
+    # -- pa_search ------------------------------------------------------------
+    def search(self, queries, k=10, ef=64, opts: SearchOpts | None = None, out=None, **kw):
+        """pa_search on HOST buffers.  `queries`/`out` may be numpy arrays or
+        (pinned) CPU torch tensors; results are written into `out`."""
+        if hasattr(queries, "data_ptr"):
+            qp, m = queries.data_ptr(), int(queries.shape[0])
+        else:
+            q = _c(queries, np.float32)
+            qp, m = _ptr(q), q.shape[0]
+        if out is None:
+            out = (np.empty((m, k), np.int32), np.empty((m, k), np.float32))
+        op = [o.data_ptr() if hasattr(o, "data_ptr") else _ptr(o) for o in out]
+        o = opts if opts is not None else make_opts(**kw)
+        _check(lib().pa_search(self._h, qp, m, k, ef, C.byref(o), op[0], op[1]))
+        return out
+
+    def search_candidates(self, queries, ef=64, opts: SearchOpts | None = None, **kw):
+        q = _c(queries, np.float32)
+        m = q.shape[0]
+        ids = np.empty((m, ef), np.int32)
+        d = np.empty((m, ef), np.float32)
+        o = opts if opts is not None else make_opts(**kw)
+        _check(lib().pa_search_candidates(self._h, _ptr(q), m, ef, C.byref(o), _ptr(ids), _ptr(d)))
+        return ids, d
+
+    # -- pa_search_device (torch CUDA tensors; pointers only) ----------------
+    def search_device(self, q, k, ef, out_ids, out_d, opts: SearchOpts | None = None, debug: Debug | None = None,
+                      stream=None, **kw):
+        o = opts if opts is not None else make_opts(**kw)
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(q.device).cuda_stream
+        _check(lib().pa_search_device(self._h, C.c_void_p(q.data_ptr()), int(q.shape[0]), k, ef, C.byref(o),
+                                      C.c_void_p(out_ids.data_ptr()), C.c_void_p(out_d.data_ptr()),
+                                      C.byref(debug) if debug is not None else None, C.c_void_p(stream)))
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().pa_get_stats(self._h, C.byref(s), C.sizeof(Stats)))
+        return s.asdict()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().pa_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def debug_buffers(m, ef, E, trace_cap=0, device="cuda"):
+    """Allocate torch device buffers for pa_debug and return (Debug struct, dict of tensors)."""
+    import torch
+    t = dict(cell=torch.empty(m, dtype=torch.int32, device=device),
+             entries=torch.empty(m, E, dtype=torch.int32, device=device),
+             cand_ids=torch.empty(m, ef, dtype=torch.int32, device=device),
+             cand_dists=torch.empty(m, ef, dtype=torch.float32, device=device),
+             counters=torch.zeros(m, 4, dtype=torch.int32, device=device))
+    if trace_cap:
+        t.update(trace_expand=torch.full((m, trace_cap), -1, dtype=torch.int32, device=device),
+                 trace_visit=torch.full((m, trace_cap), -1, dtype=torch.int32, device=device),
+                 trace_nexp=torch.zeros(m, dtype=torch.int32, device=device),
+                 trace_nvis=torch.zeros(m, dtype=torch.int32, device=device))
+    d = Debug(cell=t["cell"].data_ptr(), entries=t["entries"].data_ptr(), cand_ids=t["cand_ids"].data_ptr(),
+              cand_dists=t["cand_dists"].data_ptr(), counters=t["counters"].data_ptr(), trace_cap=trace_cap)
+    if trace_cap:
+        d.trace_expand = t["trace_expand"].data_ptr()
+        d.trace_visit = t["trace_visit"].data_ptr()
+        d.trace_nexp = t["trace_nexp"].data_ptr()
+        d.trace_nvis = t["trace_nvis"].data_ptr()
+    return d, t

@@ -1,0 +1,119 @@
+// Device helpers shared by the product kernels (NOT by the oracle).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pa {
+
+constexpr uint64_t kKeyInf = ~0ull;
+constexpr unsigned kFull = 0xffffffffu;
+
+// Orderable 32-bit image of an fp32 distance: unsigned order == float order.
+// −0.0 is canonicalised to +0.0 so that equal distances compare equal (Q13).
+__device__ __forceinline__ uint32_t ord_of(float d) {
+    uint32_t b = __float_as_uint(d == 0.0f ? 0.0f : d);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float dist_of_ord(uint32_t o) {
+    uint32_t b = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    return __uint_as_float(b);
+}
+// Candidate key: (ord(δ) << 32) | (id << 1) | checked.  Keys
+// order by (δ, id) — the oracle's (δ, id) lexicographic order (Q13).
+__device__ __forceinline__ uint64_t make_key(float d, int32_t id) {
+    return ((uint64_t)ord_of(d) << 32) | ((uint64_t)(uint32_t)id << 1);
+}
+__device__ __forceinline__ int32_t key_id(uint64_t k) { return (int32_t)(((uint32_t)k) >> 1); }
+__device__ __forceinline__ float key_dist(uint64_t k) { return dist_of_ord((uint32_t)(k >> 32)); }
+__device__ __forceinline__ bool key_checked(uint64_t k) { return (k & 1ull) != 0; }
+
+__device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int m) {
+    uint32_t lo = __shfl_xor_sync(kFull, (uint32_t)v, m);
+    uint32_t hi = __shfl_xor_sync(kFull, (uint32_t)(v >> 32), m);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+// Ascending bitonic sort of one 64-bit key per lane across the warp.
+__device__ __forceinline__ uint64_t warp_sort32(uint64_t x, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            uint64_t y = shfl_xor64(x, j);
+            bool up = (lane & k) == 0;
+            bool lower = (lane & j) == 0;
+            bool take_min = (lower == up);
+            uint64_t mn = x < y ? x : y, mx = x < y ? y : x;
+            x = take_min ? mn : mx;
+        }
+    }
+    return x;
+}
+
+// Number of elements of sorted smem array a[0..n) strictly less than x.
+__device__ __forceinline__ int lower_bound_smem(const uint64_t* a, int n, uint64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Merge the warp-sorted keys `x` (nnew valid, ascending across lanes 0..nnew)
+// into the sorted list A[0..csz) keeping the `cap` smallest; result in B.
+// Rank-based: every key lands at (own index + rank in the other list).  Keys
+// are unique (distinct ids), so the two rank counts partition positions.
+// N is a 32-entry smem scratch.  Returns the new size.
+__device__ __forceinline__ int warp_merge(const uint64_t* A, int csz, uint64_t x, int nnew,
+                                          uint64_t* B, uint64_t* N, int cap, int lane) {
+    N[lane] = x;
+    __syncwarp();
+    if (lane < nnew) {
+        int pos = lane + lower_bound_smem(A, csz, x);
+        if (pos < cap) B[pos] = x;
+    }
+    for (int i = lane; i < csz; i += 32) {
+        uint64_t a = A[i];
+        int pos = i + lower_bound_smem(N, nnew, a);
+        if (pos < cap) B[pos] = a;
+    }
+    __syncwarp();
+    int ns = csz + nnew;
+    return ns < cap ? ns : cap;
+}
+
+// Direct-form distance (Alg 1 l.8) between an smem query row and a global row
+// of `dps` floats (multiple of 4, 16-B aligned): L2 = Σ(x−q)², IP = −Σ x·q.
+// Four independent fp32 FMA chains over float4 slices (Q24: fp32, RNE, FMA).
+template <int METRIC>
+__device__ __forceinline__ float row_dist(const float* __restrict__ qs, const float* __restrict__ x, int dps) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const float4* q4 = reinterpret_cast<const float4*>(qs);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    const int n4 = dps >> 2;
+#pragma unroll 4
+    for (int i = 0; i < n4; ++i) {
+        float4 v = __ldg(x4 + i);
+        float4 w = q4[i];
+        if (METRIC == 0) {
+            float d0 = v.x - w.x, d1 = v.y - w.y, d2 = v.z - w.z, d3 = v.w - w.w;
+            a0 = fmaf(d0, d0, a0); a1 = fmaf(d1, d1, a1); a2 = fmaf(d2, d2, a2); a3 = fmaf(d3, d3, a3);
+        } else {
+            a0 = fmaf(v.x, w.x, a0); a1 = fmaf(v.y, w.y, a1); a2 = fmaf(v.z, w.z, a2); a3 = fmaf(v.w, w.w, a3);
+        }
+    }
+    float s = (a0 + a1) + (a2 + a3);
+    return METRIC == 0 ? s : -s;
+}
+
+__device__ __forceinline__ uint64_t warp_min64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t w = shfl_xor64(v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+}  // namespace pa

@@ -1,0 +1,34 @@
+// Host stages ②③ interface (internal).
+#pragma once
+#include <cstdint>
+
+namespace pa {
+
+struct HostGraph {
+    const int64_t* off = nullptr;
+    const int32_t* nb = nullptr;
+};
+
+struct HostStageArgs {
+    int32_t dim = 0, rdim = 0, metric = 0;
+    HostGraph sub, full;
+    const float* rotated = nullptr;     // X̂ [n][dim]
+    int64_t m = 0;
+    int32_t k = 10, ef1 = 64, ef2 = 32, ef3 = 64;
+    long refine_iters = 2;
+    uint32_t flags = 0;
+    int threads = 0;
+    const int32_t* cand_ids = nullptr;  // [m][ef1] stage-① C
+    const float* cand_d = nullptr;      // [m][ef1] δ' (fp32, from the GPU)
+    const float* qp = nullptr;          // [m][qp_stride] q'
+    int32_t qp_stride = 0;
+    const float* qres = nullptr;        // [m][dim − rdim]
+    int32_t* out_ids = nullptr;         // [m][k]
+    float* out_d = nullptr;             // [m][k]
+    int64_t* sum_n_dist2 = nullptr;
+    int64_t* sum_n_dist3 = nullptr;
+};
+
+void run_host_stages(const HostStageArgs& a);
+
+}  // namespace pa

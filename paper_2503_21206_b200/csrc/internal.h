@@ -1,0 +1,59 @@
+// Internal launch interfaces between the runtime (pilotann.cpp) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pa {
+
+// Device-resident replica of one index (SURVEY §8.a layouts).
+struct DevIndex {
+    int64_t n = 0;
+    int32_t dim = 0, rdim = 0, rdim_pad = 0;   // row stride of reduced vectors (multiple of 4 floats)
+    int32_t ell_w = 32;                        // ELL row width (32 or 64), −1 padded
+    int32_t metric = 0;                        // 0 L2, 1 IP
+    int32_t fes_r = 0;
+    int64_t pool_n = 0;
+    float* basis = nullptr;                    // [dim][dim] row-major V
+    float* reduced = nullptr;                  // [n][rdim_pad] (non-members: zero rows)
+    int32_t* ell = nullptr;                    // [n][ell_w]
+    float* centroids = nullptr;                // [r][rdim_pad]
+    int32_t* cell_off = nullptr;               // [r+1]
+    int32_t* pool_ids = nullptr;               // [pool_n] grouped by cell
+    float* pool_vec = nullptr;                 // [pool_n][rdim_pad] contiguous by cell
+};
+
+struct SearchArgs {
+    int64_t m = 0;
+    int32_t k = 10, ef = 64, E = 64;
+    uint32_t flags = 0;
+    int32_t hash_log2 = 12;
+    const float* q = nullptr;      // [m][dim]
+    float* qp = nullptr;           // [m][rdim_pad]  projected q'
+    float* qres = nullptr;         // [m][dim − rdim] (optional) residual projection for host stages
+    int32_t* cell = nullptr;       // [m]
+    int32_t* entries = nullptr;    // [m][E]
+    int32_t* cand_ids = nullptr;   // [m][ef] (optional)
+    float* cand_d = nullptr;       // [m][ef] (optional)
+    int32_t* out_ids = nullptr;    // [m][k]
+    float* out_d = nullptr;        // [m][k]
+    int32_t* counters = nullptr;   // [m][4] (optional)
+    int32_t* work = nullptr;       // work counter (device int, zeroed by the launcher)
+    uint64_t* spill = nullptr;     // [slots_total] epoch-tagged global overflow hash
+    int32_t spill_log2 = 16;       // per-warp slab slots = 2^spill_log2
+    int64_t spill_warps = 0;       // number of per-warp slabs available
+    uint32_t epoch_base = 1;       // level-2 slot tags: epoch = epoch_base + query index (never 0)
+    // trace
+    int32_t trace_cap = 0;
+    int32_t* trace_expand = nullptr;
+    int32_t* trace_visit = nullptr;
+    int32_t* trace_nexp = nullptr;
+    int32_t* trace_nvis = nullptr;
+};
+
+// kernels (each returns the number of kernel launches it enqueued)
+int launch_project(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
+int launch_fes(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
+int launch_traverse(const DevIndex& ix, const SearchArgs& a, int grid_warps, cudaStream_t s);
+int traverse_max_warps(const DevIndex& ix, const SearchArgs& a);   // resident warps for the launch config
+
+}  // namespace pa

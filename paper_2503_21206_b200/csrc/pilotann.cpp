@@ -1,0 +1,623 @@
+// C-ABI runtime of the B200-native PilotANN GPU stage (include/pilotann.h).
+// Validation → device replica (ELL subgraph, reduced vectors, FES pool grouped
+// by cell) → per-search pipeline: H2D → a1 projection → a2/a4 FES → a5/a6
+// traversal → a7 D2H [→ a8/a9 host stages].
+#include "pilotann.h"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_set>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "host_stages.h"
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+pa_status fail(pa_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CU(expr)                                                                                 \
+    do {                                                                                         \
+        cudaError_t e_ = (expr);                                                                 \
+        if (e_ != cudaSuccess) {                                                                 \
+            return fail(e_ == cudaErrorMemoryAllocation ? PA_ENOMEM : PA_ECUDA, "%s: %s (%s:%d)", \
+                        #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                      \
+        }                                                                                        \
+    } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+    return cudaMalloc((void**)p, std::max<size_t>(1, count) * sizeof(T));
+}
+
+std::mutex g_reg_mu;
+std::unordered_set<const void*> g_live;   // live handles (double destroy / use-after-destroy guard)
+
+int threads_default(int req) {
+    if (req > 0) return req;
+    if (const char* s = std::getenv("PILOTANN_HOST_THREADS")) {
+        int v = std::atoi(s);
+        if (v > 0) return v;
+    }
+    return (int)std::max(1u, std::thread::hardware_concurrency());
+}
+
+template <class F>
+void parallel_rows(int64_t n, F f) {
+    int T = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), std::max<int64_t>(1, n / 65536 + 1));
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t)
+        th.emplace_back([=]() { f(n * t / T, n * (t + 1) / T); });
+    for (auto& x : th) x.join();
+}
+
+// Validate a CSR over n nodes: S:L183-186.  Returns 0 or an error message code.
+pa_status check_csr(const int64_t* off, const int32_t* nb, int64_t n, int32_t max_degree, const char* what) {
+    if (off[0] != 0) return fail(PA_EGRAPH, "%s: offsets[0] = %lld, expected 0", what, (long long)off[0]);
+    std::atomic<int64_t> bad_row{-1};
+    std::atomic<int> bad_kind{0};
+    parallel_rows(n, [&](int64_t lo, int64_t hi) {
+        std::vector<int32_t> tmp;
+        for (int64_t u = lo; u < hi && bad_row.load() < 0; ++u) {
+            int64_t a = off[u], b = off[u + 1];
+            if (b < a) { bad_kind = 1; bad_row = u; return; }
+            if (max_degree > 0 && b - a > max_degree) { bad_kind = 2; bad_row = u; return; }
+            tmp.assign(nb + a, nb + b);
+            for (int32_t v : tmp)
+                if (v < 0 || v >= n) { bad_kind = 3; bad_row = u; return; }
+                else if (v == u) { bad_kind = 4; bad_row = u; return; }
+            std::sort(tmp.begin(), tmp.end());
+            for (size_t i = 1; i < tmp.size(); ++i)
+                if (tmp[i] == tmp[i - 1]) { bad_kind = 5; bad_row = u; return; }
+        }
+    });
+    if (bad_row.load() >= 0) {
+        static const char* kinds[] = {"", "offsets not monotone", "degree exceeds max_degree",
+                                      "neighbour id out of range", "self-loop", "duplicate neighbour"};
+        return fail(PA_EGRAPH, "%s: %s at node %lld", what, kinds[bad_kind.load()], (long long)bad_row.load());
+    }
+    return PA_OK;
+}
+
+int default_hash_log2(int ef) { return ef <= 64 ? 12 : 13; }
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+struct pa_index {
+    static constexpr uint32_t kMagic = 0x50414e4eu;   // "PANN"
+    uint32_t magic = kMagic;
+    int device = 0;
+    pa::DevIndex dev;
+    std::vector<int64_t> h_sub_off;        // host copy of the subgraph for stage ②
+    std::vector<int32_t> h_sub_nb;
+    const int64_t* h_full_off = nullptr;   // borrowed (pa_attach_host)
+    const int32_t* h_full_nb = nullptr;
+    const float* h_rotated = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::mutex mu;
+    pa_stats stats{};
+    bool events_pending = false;
+    // workspace
+    int64_t ws_m = 0;
+    int32_t ws_E = 0, ws_ef = 0, ws_k = 0;
+    float *q = nullptr, *qp = nullptr, *qres = nullptr, *cand_d = nullptr, *out_d = nullptr;
+    int32_t *cell = nullptr, *entries = nullptr, *cand_ids = nullptr, *out_ids = nullptr, *counters = nullptr,
+            *work = nullptr;
+    uint64_t* spill = nullptr;
+    int64_t spill_warps = 0;
+    int32_t spill_log2 = 16;
+    uint32_t epoch_base = 1;
+    // pinned host staging for the host stages
+    int64_t h_m = 0;
+    int32_t h_ef = 0;
+    int32_t *h_cand_ids = nullptr, *h_counters = nullptr;
+    float *h_cand_d = nullptr, *h_qp = nullptr, *h_qres = nullptr;
+};
+
+namespace {
+
+bool live(const pa_index* ix) {
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    return ix && g_live.count(ix) && ix->magic == pa_index::kMagic;
+}
+
+void free_ws(pa_index* ix) {
+    cudaFree(ix->q); cudaFree(ix->qp); cudaFree(ix->qres); cudaFree(ix->cand_d); cudaFree(ix->out_d);
+    cudaFree(ix->cell); cudaFree(ix->entries); cudaFree(ix->cand_ids); cudaFree(ix->out_ids);
+    cudaFree(ix->counters); cudaFree(ix->work);
+    ix->q = ix->qp = ix->qres = ix->cand_d = ix->out_d = nullptr;
+    ix->cell = ix->entries = ix->cand_ids = ix->out_ids = ix->counters = ix->work = nullptr;
+    ix->ws_m = 0;
+}
+
+pa_status ensure_ws(pa_index* ix, int64_t m, int32_t E, int32_t ef, int32_t k) {
+    if (m <= ix->ws_m && E <= ix->ws_E && ef <= ix->ws_ef && k <= ix->ws_k) return PA_OK;
+    free_ws(ix);
+    m = std::max<int64_t>(m, 1);
+    E = std::max(E, ix->ws_E); ef = std::max(ef, ix->ws_ef); k = std::max(k, ix->ws_k);
+    const auto& d = ix->dev;
+    CU(dalloc(&ix->q, (size_t)m * d.dim));
+    CU(dalloc(&ix->qp, (size_t)m * d.rdim_pad));
+    CU(dalloc(&ix->qres, (size_t)m * std::max(1, d.dim - d.rdim)));
+    CU(dalloc(&ix->cell, (size_t)m));
+    CU(dalloc(&ix->entries, (size_t)m * E));
+    CU(dalloc(&ix->cand_ids, (size_t)m * ef));
+    CU(dalloc(&ix->cand_d, (size_t)m * ef));
+    CU(dalloc(&ix->out_ids, (size_t)m * k));
+    CU(dalloc(&ix->out_d, (size_t)m * k));
+    CU(dalloc(&ix->counters, (size_t)m * 4));
+    CU(dalloc(&ix->work, 4));
+    ix->ws_m = m; ix->ws_E = E; ix->ws_ef = ef; ix->ws_k = k;
+    return PA_OK;
+}
+
+pa_status ensure_spill(pa_index* ix, int64_t warps) {
+    if (warps <= ix->spill_warps) return PA_OK;
+    cudaFree(ix->spill);
+    ix->spill = nullptr;
+    ix->spill_warps = 0;
+    size_t bytes = (size_t)warps * ((size_t)8 << ix->spill_log2);
+    CU(cudaMalloc((void**)&ix->spill, bytes));
+    CU(cudaMemset(ix->spill, 0, bytes));
+    ix->spill_warps = warps;
+    ix->epoch_base = 1;
+    return PA_OK;
+}
+
+struct Resolved {
+    int32_t stages, ef1, ef2, ef3, E, width, refine, hash_log2, threads;
+    uint32_t flags;
+};
+
+pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r) {
+    pa_search_opts z{};
+    if (!o) o = &z;
+    r->stages = o->stages ? o->stages : PA_STAGES_GPU;
+    if (r->stages != PA_STAGES_GPU && r->stages != PA_STAGES_FULL) return fail(PA_EINVAL, "bad stages %d", r->stages);
+    if (k < 1) return fail(PA_EINVAL, "k = %d < 1", k);
+    if (ef < k) return fail(PA_EINVAL, "ef = %d < k = %d", ef, k);
+    r->ef1 = o->ef1 ? o->ef1 : ef;
+    r->ef3 = o->ef3 ? o->ef3 : ef;
+    r->ef2 = o->ef2 ? o->ef2 : std::max(k, ef / 2);
+    r->E = o->entries ? o->entries : r->ef1;
+    r->width = o->width ? o->width : 1;
+    r->refine = o->refine_iters == 0 ? 2 : (o->refine_iters < 0 ? 0 : o->refine_iters);
+    r->flags = o->flags;
+    r->hash_log2 = o->hash_slots_log2 ? o->hash_slots_log2 : default_hash_log2(r->ef1);
+    r->threads = threads_default(o->host_threads);
+    if (r->ef1 > 256 || r->ef2 > 256 || r->ef3 > 256) return fail(PA_EINVAL, "ef > 256");
+    if (r->ef1 < 1 || r->ef2 < 1 || r->ef3 < 1 || r->E < 1 || r->E > 1024) return fail(PA_EINVAL, "bad ef/entries");
+    if (r->stages == PA_STAGES_GPU && k > r->ef1) return fail(PA_EINVAL, "k = %d > ef1 = %d", k, r->ef1);
+    if (r->stages == PA_STAGES_FULL && (k > r->ef3 || k > r->ef2)) return fail(PA_EINVAL, "k > ef2/ef3");
+    if (r->width != 1) return fail(PA_ENOTSUP, "search width w = %d: only w = 1 on the GPU", r->width);
+    if (r->hash_log2 < 5 || r->hash_log2 > 15) return fail(PA_EINVAL, "hash_slots_log2 = %d", r->hash_log2);
+    return PA_OK;
+}
+
+// Enqueue a1..a6 on stream s for device queries q → out ids/dists.
+pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k, const Resolved& r,
+                            int32_t* d_out_ids, float* d_out_d, const pa_debug* dbg, bool want_qres,
+                            cudaStream_t s) {
+    pa_status st = ensure_ws(ix, m, r.E, r.ef1, k);
+    if (st != PA_OK) return st;
+    pa::SearchArgs a;
+    a.m = m; a.k = k; a.ef = r.ef1; a.E = r.E; a.flags = r.flags; a.hash_log2 = r.hash_log2;
+    a.q = d_q; a.qp = ix->qp; a.qres = want_qres ? ix->qres : nullptr;
+    a.cell = (dbg && dbg->cell) ? dbg->cell : ix->cell;
+    a.entries = (dbg && dbg->entries) ? dbg->entries : ix->entries;
+    a.cand_ids = (dbg && dbg->cand_ids) ? dbg->cand_ids : ix->cand_ids;
+    a.cand_d = (dbg && dbg->cand_dists) ? dbg->cand_dists : ix->cand_d;
+    a.counters = (dbg && dbg->counters) ? dbg->counters : ix->counters;
+    a.out_ids = d_out_ids; a.out_d = d_out_d;
+    a.work = ix->work;
+    if (dbg && dbg->trace_cap > 0 && dbg->trace_expand && dbg->trace_visit && dbg->trace_nexp && dbg->trace_nvis) {
+        a.trace_cap = dbg->trace_cap; a.trace_expand = dbg->trace_expand; a.trace_visit = dbg->trace_visit;
+        a.trace_nexp = dbg->trace_nexp; a.trace_nvis = dbg->trace_nvis;
+    }
+    int maxw = pa::traverse_max_warps(ix->dev, a);
+    if (maxw <= 0) return fail(PA_ENOTSUP, "traversal does not fit on an SM (ef=%d, hash_log2=%d)", r.ef1, r.hash_log2);
+    int64_t gridw = std::min<int64_t>(maxw, ((m + 3) / 4) * 4);
+    st = ensure_spill(ix, gridw);
+    if (st != PA_OK) return st;
+    if ((uint64_t)ix->epoch_base + (uint64_t)m + 1 >= 0xffffffffull) {
+        CU(cudaMemsetAsync(ix->spill, 0, (size_t)ix->spill_warps * ((size_t)8 << ix->spill_log2), s));
+        ix->epoch_base = 1;
+    }
+    a.spill = ix->spill; a.spill_log2 = ix->spill_log2; a.spill_warps = ix->spill_warps;
+    a.epoch_base = ix->epoch_base;
+    ix->epoch_base += (uint32_t)m + 1;
+
+    int launches = 0;
+    CU(cudaEventRecord(ix->ev[0], s));
+    launches += pa::launch_project(ix->dev, a, s);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(ix->ev[1], s));
+    launches += pa::launch_fes(ix->dev, a, s);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(ix->ev[2], s));
+    launches += pa::launch_traverse(ix->dev, a, (int)gridw, s);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(ix->ev[3], s));
+    ix->events_pending = true;
+    ix->stats = pa_stats{};
+    ix->stats.queries = m;
+    ix->stats.kernel_launches = launches;
+    return PA_OK;
+}
+
+void collect_event_times(pa_index* ix) {
+    if (!ix->events_pending) return;
+    cudaEventSynchronize(ix->ev[3]);
+    float t01 = 0, t12 = 0, t23 = 0, t03 = 0;
+    cudaEventElapsedTime(&t01, ix->ev[0], ix->ev[1]);
+    cudaEventElapsedTime(&t12, ix->ev[1], ix->ev[2]);
+    cudaEventElapsedTime(&t23, ix->ev[2], ix->ev[3]);
+    cudaEventElapsedTime(&t03, ix->ev[0], ix->ev[3]);
+    ix->stats.ms_project = t01; ix->stats.ms_fes = t12; ix->stats.ms_traverse = t23; ix->stats.ms_total_gpu = t03;
+    ix->events_pending = false;
+}
+
+pa_status ensure_host_ws(pa_index* ix, int64_t m, int32_t ef) {
+    if (m <= ix->h_m && ef <= ix->h_ef) return PA_OK;
+    cudaFreeHost(ix->h_cand_ids); cudaFreeHost(ix->h_cand_d); cudaFreeHost(ix->h_qp); cudaFreeHost(ix->h_qres);
+    cudaFreeHost(ix->h_counters);
+    ix->h_cand_ids = nullptr; ix->h_cand_d = ix->h_qp = ix->h_qres = nullptr; ix->h_counters = nullptr;
+    ix->h_m = 0;
+    const auto& d = ix->dev;
+    CU(cudaMallocHost((void**)&ix->h_cand_ids, sizeof(int32_t) * m * ef));
+    CU(cudaMallocHost((void**)&ix->h_cand_d, sizeof(float) * m * ef));
+    CU(cudaMallocHost((void**)&ix->h_qp, sizeof(float) * m * d.rdim_pad));
+    CU(cudaMallocHost((void**)&ix->h_qres, sizeof(float) * m * std::max(1, d.dim - d.rdim)));
+    CU(cudaMallocHost((void**)&ix->h_counters, sizeof(int32_t) * m * 4));
+    ix->h_m = m; ix->h_ef = ef;
+    return PA_OK;
+}
+
+}  // namespace
+
+// ============================================================================ ABI
+extern "C" {
+
+const char* pa_last_error(void) { return g_err.c_str(); }
+const char* pa_version(void) { return "pilotann-b200 0.1 (sm_100a)"; }
+
+pa_status pa_build(const pa_build_params* p, pa_index** out) {
+    g_err.clear();
+    if (!p || !out) return fail(PA_EINVAL, "null argument");
+    *out = nullptr;
+    if (!p->sub_offsets || !p->reduced || !p->basis || !p->fes_centroids || !p->fes_cell_off || !p->fes_pool_ids)
+        return fail(PA_EINVAL, "null input array");
+    if (p->n <= 0 || p->n >= (1ll << 31)) return fail(PA_EINVAL, "n = %lld out of range", (long long)p->n);
+    if (p->sub_offsets[p->n] > 0 && !p->sub_neighbors) return fail(PA_EINVAL, "null sub_neighbors");
+    if (p->dim <= 0 || p->rdim <= 0 || p->rdim > p->dim) return fail(PA_EINVAL, "bad dims D=%d d'=%d", p->dim, p->rdim);
+    if (p->dim > 4096) return fail(PA_EINVAL, "dim %d > 4096", p->dim);
+    if (p->max_degree < 1 || p->max_degree > 64) return fail(PA_EINVAL, "max_degree %d not in 1..64", p->max_degree);
+    if (p->metric != PA_L2 && p->metric != PA_IP) return fail(PA_EINVAL, "bad metric %d", p->metric);
+    if (p->fes_r < 1 || p->fes_r > 1024) return fail(PA_EINVAL, "fes_r %d not in 1..1024", p->fes_r);
+    const int64_t n = p->n;
+    const int D = p->dim, dp = p->rdim;
+    // ---- graph and subgraph invariants
+    pa_status st = check_csr(p->sub_offsets, p->sub_neighbors, n, p->max_degree, "subgraph");
+    if (st != PA_OK) return st;
+    std::vector<uint8_t> member(n);
+    for (int64_t u = 0; u < n; ++u) {
+        bool deg = p->sub_offsets[u + 1] > p->sub_offsets[u];
+        member[u] = p->member_flags ? (p->member_flags[u] != 0) : deg;
+        if (!member[u] && deg) return fail(PA_EGRAPH, "non-member %lld has out-edges", (long long)u);
+    }
+    for (int64_t e = 0; e < p->sub_offsets[n]; ++e)
+        if (!member[p->sub_neighbors[e]])
+            return fail(PA_EGRAPH, "edge into non-member %d", p->sub_neighbors[e]);
+    // ---- basis orthonormal and finite
+    for (int64_t i = 0; i < (int64_t)D * D; ++i)
+        if (!std::isfinite(p->basis[i])) return fail(PA_EINVAL, "non-finite basis entry %lld", (long long)i);
+    {
+        double worst = 0;
+        std::vector<double> col((size_t)D * D);
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) col[(size_t)j * D + i] = p->basis[(size_t)i * D + j];
+        for (int a = 0; a < D; ++a)
+            for (int b = a; b < D; ++b) {
+                double s = 0;
+                const double* ca = &col[(size_t)a * D];
+                const double* cb = &col[(size_t)b * D];
+                for (int i = 0; i < D; ++i) s += ca[i] * cb[i];
+                worst = std::max(worst, std::fabs(s - (a == b ? 1.0 : 0.0)));
+            }
+        if (worst > 1e-4) return fail(PA_EBASIS, "basis not orthonormal: max|VtV-I| = %.3g", worst);
+    }
+    for (int64_t u = 0; u < n; ++u)
+        if (member[u])
+            for (int j = 0; j < dp; ++j)
+                if (!std::isfinite(p->reduced[u * dp + j])) return fail(PA_EINVAL, "non-finite reduced[%lld]", (long long)u);
+    // ---- FES index
+    const int r = p->fes_r;
+    if (p->fes_cell_off[0] != 0) return fail(PA_EFES, "fes_cell_off[0] != 0");
+    for (int c = 0; c < r; ++c)
+        if (p->fes_cell_off[c + 1] <= p->fes_cell_off[c]) return fail(PA_EFES, "FES cell %d is empty", c);
+    const int64_t pool_n = p->fes_cell_off[r];
+    if (pool_n >= (1ll << 31)) return fail(PA_EFES, "pool too large");
+    {
+        std::vector<uint8_t> seen(n, 0);
+        for (int64_t j = 0; j < pool_n; ++j) {
+            int32_t e = p->fes_pool_ids[j];
+            if (e < 0 || e >= n) return fail(PA_EFES, "pool id %d out of range", e);
+            if (!member[e]) return fail(PA_EFES, "pool id %d is not a member", e);
+            if (seen[e]) return fail(PA_EFES, "pool id %d duplicated", e);
+            seen[e] = 1;
+        }
+    }
+    for (int64_t i = 0; i < (int64_t)r * dp; ++i)
+        if (!std::isfinite(p->fes_centroids[i])) return fail(PA_EINVAL, "non-finite centroid");
+
+    // ---- device replica
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (p->device < 0 || p->device >= ndev) return fail(PA_EINVAL, "device %d not in [0,%d)", p->device, ndev);
+    CU(cudaSetDevice(p->device));
+    int major = 0, minor = 0;
+    CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, p->device));
+    CU(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, p->device));
+    if (major != 10 || minor != 0)
+        return fail(PA_ENOTSUP, "device %d is sm_%d%d; this library is built for sm_100a only", p->device, major, minor);
+
+    pa_index* ix = new pa_index();
+    ix->device = p->device;
+    auto& d = ix->dev;
+    d.n = n; d.dim = D; d.rdim = dp; d.rdim_pad = (dp + 3) & ~3; d.metric = p->metric; d.fes_r = r;
+    d.pool_n = pool_n;
+    d.ell_w = p->max_degree <= 32 ? 32 : 64;
+    const int dps = d.rdim_pad;
+    auto bail = [&](pa_status s) { pa_destroy(ix); return s; };
+    {
+        std::lock_guard<std::mutex> g(g_reg_mu);
+        g_live.insert(ix);
+    }
+#define CUB(expr)                                                                                  \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return bail(fail(e_ == cudaErrorMemoryAllocation ? PA_ENOMEM : PA_ECUDA, "%s: %s", #expr, \
+                             cudaGetErrorString(e_)));                                             \
+    } while (0)
+    CUB(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+    for (auto& e : ix->ev) CUB(cudaEventCreate(&e));
+    CUB(dalloc(&d.basis, (size_t)D * D));
+    CUB(cudaMemcpy(d.basis, p->basis, sizeof(float) * D * D, cudaMemcpyHostToDevice));
+    // reduced vectors [n][dps] (zero rows for non-members), staged in chunks
+    CUB(dalloc(&d.reduced, (size_t)n * dps));
+    CUB(dalloc(&d.ell, (size_t)n * d.ell_w));
+    {
+        const int64_t chunk = 1 << 20;
+        std::vector<float> rb((size_t)std::min(chunk, n) * dps);
+        std::vector<int32_t> eb((size_t)std::min(chunk, n) * d.ell_w);
+        for (int64_t s0 = 0; s0 < n; s0 += chunk) {
+            int64_t s1 = std::min(n, s0 + chunk);
+            parallel_rows(s1 - s0, [&](int64_t lo, int64_t hi) {
+                for (int64_t i = lo; i < hi; ++i) {
+                    int64_t u = s0 + i;
+                    float* dst = &rb[(size_t)i * dps];
+                    if (member[u]) {
+                        std::memcpy(dst, p->reduced + u * dp, sizeof(float) * dp);
+                        for (int j = dp; j < dps; ++j) dst[j] = 0.f;
+                    } else {
+                        std::memset(dst, 0, sizeof(float) * dps);
+                    }
+                    int32_t* row = &eb[(size_t)i * d.ell_w];
+                    int64_t a0 = p->sub_offsets[u], a1 = p->sub_offsets[u + 1];
+                    for (int j = 0; j < d.ell_w; ++j) row[j] = (a0 + j < a1) ? p->sub_neighbors[a0 + j] : -1;
+                }
+            });
+            CUB(cudaMemcpy(d.reduced + s0 * dps, rb.data(), sizeof(float) * (s1 - s0) * dps, cudaMemcpyHostToDevice));
+            CUB(cudaMemcpy(d.ell + s0 * d.ell_w, eb.data(), sizeof(int32_t) * (s1 - s0) * d.ell_w, cudaMemcpyHostToDevice));
+        }
+    }
+    // FES: centroids, cell offsets, pool ids and pool vectors grouped by cell
+    {
+        std::vector<float> cb((size_t)r * dps, 0.f);
+        for (int c = 0; c < r; ++c) std::memcpy(&cb[(size_t)c * dps], p->fes_centroids + (size_t)c * dp, sizeof(float) * dp);
+        CUB(dalloc(&d.centroids, cb.size()));
+        CUB(cudaMemcpy(d.centroids, cb.data(), sizeof(float) * cb.size(), cudaMemcpyHostToDevice));
+        std::vector<int32_t> co(r + 1);
+        for (int c = 0; c <= r; ++c) co[c] = (int32_t)p->fes_cell_off[c];
+        CUB(dalloc(&d.cell_off, co.size()));
+        CUB(cudaMemcpy(d.cell_off, co.data(), sizeof(int32_t) * co.size(), cudaMemcpyHostToDevice));
+        CUB(dalloc(&d.pool_ids, (size_t)pool_n));
+        CUB(cudaMemcpy(d.pool_ids, p->fes_pool_ids, sizeof(int32_t) * pool_n, cudaMemcpyHostToDevice));
+        std::vector<float> pv((size_t)pool_n * dps, 0.f);
+        for (int64_t j = 0; j < pool_n; ++j)
+            std::memcpy(&pv[(size_t)j * dps], p->reduced + (int64_t)p->fes_pool_ids[j] * dp, sizeof(float) * dp);
+        CUB(dalloc(&d.pool_vec, pv.size()));
+        CUB(cudaMemcpy(d.pool_vec, pv.data(), sizeof(float) * pv.size(), cudaMemcpyHostToDevice));
+    }
+    ix->h_sub_off.assign(p->sub_offsets, p->sub_offsets + n + 1);
+    ix->h_sub_nb.assign(p->sub_neighbors, p->sub_neighbors + p->sub_offsets[n]);
+    CUB(cudaDeviceSynchronize());
+#undef CUB
+    *out = ix;
+    return PA_OK;
+}
+
+pa_status pa_attach_host(pa_index* ix, const int64_t* full_offsets, const int32_t* full_neighbors,
+                         const float* rotated_full) {
+    g_err.clear();
+    if (!live(ix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
+    if (!full_offsets || !full_neighbors || !rotated_full) return fail(PA_EINVAL, "null argument");
+    pa_status st = check_csr(full_offsets, full_neighbors, ix->dev.n, 0, "full graph");
+    if (st != PA_OK) return st;
+    std::lock_guard<std::mutex> g(ix->mu);
+    ix->h_full_off = full_offsets;
+    ix->h_full_nb = full_neighbors;
+    ix->h_rotated = rotated_full;
+    return PA_OK;
+}
+
+pa_status pa_search_device(pa_index* ix, const float* d_queries, int64_t m, int32_t k, int32_t ef,
+                           const pa_search_opts* opts, int32_t* d_out_ids, float* d_out_dists,
+                           const pa_debug* dbg, void* stream) {
+    g_err.clear();
+    if (!live(ix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
+    if (m < 0) return fail(PA_EINVAL, "m < 0");
+    if (m > 0 && (!d_queries || !d_out_ids || !d_out_dists)) return fail(PA_EINVAL, "null argument");
+    Resolved r;
+    pa_status st = resolve(opts, k, ef, &r);
+    if (st != PA_OK) return st;
+    if (r.stages != PA_STAGES_GPU) return fail(PA_EINVAL, "pa_search_device runs stage 1 only");
+    std::lock_guard<std::mutex> g(ix->mu);
+    CU(cudaSetDevice(ix->device));
+    cudaStream_t s = stream ? (cudaStream_t)stream : ix->stream;
+    if (m == 0) return PA_OK;
+    return enqueue_gpu_stage(ix, d_queries, m, k, r, d_out_ids, d_out_dists, dbg, false, s);
+}
+
+static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m, int32_t k, const Resolved& r,
+                                  int32_t* out_ids, float* out_d, bool candidates_only) {
+    auto t0 = std::chrono::steady_clock::now();
+    CU(cudaSetDevice(ix->device));
+    cudaStream_t s = ix->stream;
+    const bool full = !candidates_only && r.stages == PA_STAGES_FULL;
+    if (full && (!ix->h_rotated || !ix->h_full_off))
+        return fail(PA_ESTATE, "PA_STAGES_FULL requires pa_attach_host");
+    pa_status st = ensure_ws(ix, m, r.E, r.ef1, k);
+    if (st != PA_OK) return st;
+    const auto& d = ix->dev;
+    CU(cudaMemcpyAsync(ix->q, queries, sizeof(float) * m * d.dim, cudaMemcpyHostToDevice, s));
+    st = enqueue_gpu_stage(ix, ix->q, m, k, r, ix->out_ids, ix->out_d, nullptr, full, s);
+    if (st != PA_OK) return st;
+    const int64_t launches = ix->stats.kernel_launches;
+    if (candidates_only) {
+        CU(cudaMemcpyAsync(out_ids, ix->cand_ids, sizeof(int32_t) * m * r.ef1, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(out_d, ix->cand_d, sizeof(float) * m * r.ef1, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    } else if (!full) {
+        CU(cudaMemcpyAsync(out_ids, ix->out_ids, sizeof(int32_t) * m * k, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(out_d, ix->out_d, sizeof(float) * m * k, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+    } else {
+        st = ensure_host_ws(ix, m, r.ef1);
+        if (st != PA_OK) return st;
+        CU(cudaMemcpyAsync(ix->h_cand_ids, ix->cand_ids, sizeof(int32_t) * m * r.ef1, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(ix->h_cand_d, ix->cand_d, sizeof(float) * m * r.ef1, cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(ix->h_qp, ix->qp, sizeof(float) * m * d.rdim_pad, cudaMemcpyDeviceToHost, s));
+        if (d.dim > d.rdim)
+            CU(cudaMemcpyAsync(ix->h_qres, ix->qres, sizeof(float) * m * (d.dim - d.rdim), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        auto th = std::chrono::steady_clock::now();
+        pa::HostStageArgs h;
+        h.dim = d.dim; h.rdim = d.rdim; h.metric = d.metric;
+        h.sub.off = ix->h_sub_off.data(); h.sub.nb = ix->h_sub_nb.data();
+        h.full.off = ix->h_full_off; h.full.nb = ix->h_full_nb;
+        h.rotated = ix->h_rotated;
+        h.m = m; h.k = k; h.ef1 = r.ef1; h.ef2 = r.ef2; h.ef3 = r.ef3; h.refine_iters = r.refine;
+        h.flags = r.flags; h.threads = r.threads;
+        h.cand_ids = ix->h_cand_ids; h.cand_d = ix->h_cand_d; h.qp = ix->h_qp; h.qp_stride = d.rdim_pad;
+        h.qres = ix->h_qres; h.out_ids = out_ids; h.out_d = out_d;
+        int64_t s2 = 0, s3 = 0;
+        h.sum_n_dist2 = &s2; h.sum_n_dist3 = &s3;
+        pa::run_host_stages(h);
+        ix->stats.ms_host_stages = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th).count();
+        ix->stats.sum_n_dist2 = s2; ix->stats.sum_n_dist3 = s3;
+    }
+    collect_event_times(ix);
+    ix->stats.kernel_launches = launches;
+    ix->stats.ms_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return PA_OK;
+}
+
+pa_status pa_search(pa_index* ix, const float* queries, int64_t m, int32_t k, int32_t ef,
+                    const pa_search_opts* opts, int32_t* out_ids, float* out_dists) {
+    g_err.clear();
+    if (!live(ix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
+    if (m < 0) return fail(PA_EINVAL, "m < 0");
+    if (m > 0 && (!queries || !out_ids || !out_dists)) return fail(PA_EINVAL, "null argument");
+    Resolved r;
+    pa_status st = resolve(opts, k, ef, &r);
+    if (st != PA_OK) return st;
+    std::lock_guard<std::mutex> g(ix->mu);
+    if (m == 0) return PA_OK;
+    return search_host_impl(ix, queries, m, k, r, out_ids, out_dists, false);
+}
+
+pa_status pa_search_candidates(pa_index* ix, const float* queries, int64_t m, int32_t ef,
+                               const pa_search_opts* opts, int32_t* cand_ids, float* cand_dists) {
+    g_err.clear();
+    if (!live(ix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
+    if (m < 0) return fail(PA_EINVAL, "m < 0");
+    if (m > 0 && (!queries || !cand_ids || !cand_dists)) return fail(PA_EINVAL, "null argument");
+    Resolved r;
+    pa_status st = resolve(opts, 1, ef, &r);
+    if (st != PA_OK) return st;
+    if (opts && opts->ef1 && opts->ef1 != ef) return fail(PA_EINVAL, "candidates are [m][ef]: ef1 must equal ef");
+    std::lock_guard<std::mutex> g(ix->mu);
+    if (m == 0) return PA_OK;
+    return search_host_impl(ix, queries, m, 1, r, cand_ids, cand_dists, true);
+}
+
+pa_status pa_get_stats(const pa_index* cix, pa_stats* out, size_t size) {
+    g_err.clear();
+    if (!live(cix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
+    if (!out || size < sizeof(pa_stats)) return fail(PA_EINVAL, "bad stats buffer");
+    pa_index* ix = const_cast<pa_index*>(cix);
+    std::lock_guard<std::mutex> g(ix->mu);
+    cudaSetDevice(ix->device);
+    collect_event_times(ix);
+    // reduce stage-① counters of the last search
+    if (ix->stats.queries > 0 && ix->counters) {
+        std::vector<int32_t> c((size_t)ix->stats.queries * 4);
+        if (cudaMemcpy(c.data(), ix->counters, sizeof(int32_t) * c.size(), cudaMemcpyDeviceToHost) == cudaSuccess) {
+            int64_t se = 0, sd = 0, ss = 0, ov = 0;
+            for (int64_t q = 0; q < ix->stats.queries; ++q) {
+                se += c[q * 4]; sd += c[q * 4 + 1]; ss += c[q * 4 + 2]; ov += c[q * 4 + 3] != 0;
+            }
+            ix->stats.sum_n_exp = se; ix->stats.sum_n_dist = sd; ix->stats.sum_spill = ss; ix->stats.overflow_queries = ov;
+        }
+    }
+    std::memcpy(out, &ix->stats, sizeof(pa_stats));
+    return PA_OK;
+}
+
+void pa_destroy(pa_index* ix) {
+    {
+        std::lock_guard<std::mutex> g(g_reg_mu);
+        if (!ix || !g_live.count(ix)) return;
+        g_live.erase(ix);
+    }
+    cudaSetDevice(ix->device);
+    if (ix->stream) cudaStreamSynchronize(ix->stream);
+    free_ws(ix);
+    cudaFree(ix->spill);
+    cudaFreeHost(ix->h_cand_ids); cudaFreeHost(ix->h_cand_d); cudaFreeHost(ix->h_qp); cudaFreeHost(ix->h_qres);
+    cudaFreeHost(ix->h_counters);
+    auto& d = ix->dev;
+    cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
+    cudaFree(d.pool_ids); cudaFree(d.pool_vec);
+    for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
+    if (ix->stream) cudaStreamDestroy(ix->stream);
+    ix->magic = 0;
+    delete ix;
+}
+
+}  // extern "C"

@@ -1,0 +1,248 @@
+// a5 + a6 — stage ① traversal: Alg 1 over the sampled subgraph
+// with reduced vectors, one warp per query, persistent grid with a
+// global work counter.
+//
+// Per query (warp):
+//   C        : sorted list of ≤ ef 64-bit keys (ord(δ)<<32 | id<<1 | checked) in smem,
+//              ping-pong buffers A/B, merged by rank (common.cuh warp_merge).
+//   visited  : EXACT set (needed for Alg 1's "unvisited" test to be bit-faithful,
+//              I4) — level 1 = open-addressing int32 hash in smem (2^hash_log2
+//              slots, accepts inserts while ≤ half full); level 2 = per-warp
+//              epoch-tagged 64-bit hash slab in global memory once level 1 closes.
+//              The paper's bloom filter is NEXT-f1.
+//   loop     : u ← smallest unchecked key (warp ballot over C, Alg 1 l.5);
+//              ELL[u][lane] (one coalesced 128-B row per 32 neighbours, l.6);
+//              test-and-insert visited (l.7); new lanes gather their reduced row
+//              (float4 loads) and compute δ' in fp32 (l.8); warp bitonic sort of
+//              the ≤32 new keys and rank-merge into C truncated to ef (l.9, l.11).
+#include "common.cuh"
+#include "internal.h"
+
+namespace pa {
+
+namespace {
+constexpr int kTW = 4;                 // warps per block
+constexpr int kIterCap = 1000000;      // Q16 safety cap (status 2)
+
+__device__ __forceinline__ uint32_t hash1(int32_t v) { return (uint32_t)v * 0x9E3779B1u; }
+__device__ __forceinline__ uint32_t hash2(int32_t v) { return ((uint32_t)v ^ 0x5bd1e995u) * 0x85EBCA77u; }
+
+struct Visited {
+    volatile int32_t* H;   // smem level 1
+    int log2S;
+    int count1;            // entries in level 1 (warp-uniform)
+    uint64_t* G;           // global level 2 slab
+    uint32_t gmask;
+    uint32_t epoch;
+    int count2;            // entries in level 2 (warp-uniform)
+};
+
+// Returns true iff v was not yet visited (and is now).  `open1` is warp-uniform.
+__device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& in_l2) {
+    in_l2 = false;
+    const uint32_t S = 1u << vs.log2S;
+    uint32_t h = hash1(v) >> (32 - vs.log2S);
+    for (uint32_t p = 0; p < S; ++p) {
+        int32_t cur = vs.H[h];
+        if (cur == v) return false;
+        if (cur == -1) {
+            if (!open1) break;                                   // not in level 1
+            int32_t old = atomicCAS((int32_t*)&vs.H[h], -1, v);
+            if (old == -1) return true;
+            if (old == v) return false;
+        }
+        h = (h + 1) & (S - 1);
+    }
+    // level 2: epoch-tagged slots; a slot whose epoch differs is free
+    const uint64_t tag = ((uint64_t)vs.epoch << 32) | (uint32_t)v;
+    uint32_t g = hash2(v) & vs.gmask;
+    for (uint32_t p = 0; p <= vs.gmask; ++p) {
+        uint64_t cur = *(volatile uint64_t*)&vs.G[g];
+        while (true) {
+            if ((uint32_t)(cur >> 32) == vs.epoch) {
+                if ((uint32_t)cur == (uint32_t)v) return false;
+                break;
+            }
+            unsigned long long old = atomicCAS((unsigned long long*)&vs.G[g], (unsigned long long)cur,
+                                               (unsigned long long)tag);
+            if (old == cur) { in_l2 = true; return true; }
+            cur = old;
+        }
+        g = (g + 1) & vs.gmask;
+    }
+    return false;   // unreachable while count2 ≤ gmask/2 (guarded by the caller)
+}
+
+template <int METRIC, int ELLW, bool TRACE>
+__global__ void __launch_bounds__(kTW * 32) k_traverse(DevIndex ix, SearchArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
+    const size_t per_warp = (size_t)(2 * ef + 32) * 8 + (size_t)dps * 4 + (size_t)S * 4;
+    unsigned char* base = smem_raw + per_warp * w;
+    uint64_t* A0 = reinterpret_cast<uint64_t*>(base);
+    uint64_t* B0 = A0 + ef;
+    uint64_t* N = B0 + ef;
+    float* qs = reinterpret_cast<float*>(N + 32);
+    int32_t* H = reinterpret_cast<int32_t*>(qs + dps);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int64_t gw = (int64_t)blockIdx.x * kTW + w;
+
+    Visited vs;
+    vs.H = H;
+    vs.log2S = a.hash_log2;
+    vs.G = a.spill + ((int64_t)gw << a.spill_log2);
+    vs.gmask = (1u << a.spill_log2) - 1u;
+    const int cap1 = S >> 1, cap2 = (int)(vs.gmask >> 1);
+
+    for (;;) {
+        int64_t q = 0;
+        if (lane == 0) q = atomicAdd(a.work, 1);
+        q = __shfl_sync(kFull, (int)q, 0);
+        if (q >= a.m) break;
+        vs.epoch = a.epoch_base + (uint32_t)q;
+        vs.count1 = 0;
+        vs.count2 = 0;
+        for (int i = lane; i < dps; i += 32) qs[i] = a.qp[q * dps + i];
+        int4* H4 = reinterpret_cast<int4*>(H);
+        for (int i = lane; i < (S >> 2); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
+        __syncwarp();
+
+        uint64_t* cur = A0;
+        uint64_t* nxt = B0;
+        int csz = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
+
+        // Process one batch of ≤32 candidate ids (one per lane, −1 = none):
+        // visited test-and-insert, δ for new ids, sort, merge into C.
+        auto batch = [&](int32_t v) {
+            const bool open1 = vs.count1 + 32 <= cap1;
+            if (!open1 && vs.count2 + 32 > cap2) { status = 1; return; }
+            bool l2 = false;
+            const bool isnew = v >= 0 && visit(vs, v, open1, l2);
+            const unsigned bal = __ballot_sync(kFull, isnew);
+            const unsigned bl2 = __ballot_sync(kFull, l2);
+            const int nnew = __popc(bal);
+            if (open1) vs.count1 += nnew; else vs.count2 += __popc(bl2);
+            n_spill += __popc(bl2);
+            if (TRACE && isnew) {
+                int pos = n_dist + __popc(bal & lt_mask);
+                if (pos < a.trace_cap) a.trace_visit[q * a.trace_cap + pos] = v;
+            }
+            n_dist += nnew;
+            if (nnew == 0) return;
+            uint64_t key = kKeyInf;
+            if (isnew) key = make_key(row_dist<METRIC>(qs, ix.reduced + (int64_t)v * dps, dps), v);
+            key = warp_sort32(key, lane);
+            if (csz == ef) {                       // nothing can enter C: skip the merge
+                uint64_t k0 = ((uint64_t)__shfl_sync(kFull, (uint32_t)(key >> 32), 0) << 32) |
+                              __shfl_sync(kFull, (uint32_t)key, 0);
+                if (k0 > cur[ef - 1]) return;
+            }
+            csz = warp_merge(cur, csz, key, nnew, nxt, N, ef, lane);
+            uint64_t* t = cur; cur = nxt; nxt = t;
+        };
+
+        // ---- a5: C := entries (Alg 1 l.3), visited := entries (Q15)
+        for (int j0 = 0; j0 < a.E && status == 0; j0 += 32) {
+            int j = j0 + lane;
+            batch(j < a.E ? a.entries[q * a.E + j] : -1);
+        }
+        // ---- a6: Alg 1 l.4-12
+        if (!(a.flags & 4u)) {
+            for (int it = 0; status == 0; ++it) {
+                int p = -1;
+                for (int t = 0; t * 32 < csz; ++t) {
+                    int i = t * 32 + lane;
+                    bool un = i < csz && !key_checked(cur[i]);
+                    unsigned b = __ballot_sync(kFull, un);
+                    if (b) { p = t * 32 + __ffs(b) - 1; break; }
+                }
+                if (p < 0) break;                                   // l.12: no unchecked node
+                const uint64_t ku = cur[p];
+                const int32_t u = key_id(ku);
+                __syncwarp();
+                if (lane == 0) cur[p] = ku | 1ull;                  // mark checked
+                if (TRACE && lane == 0 && n_exp < a.trace_cap) a.trace_expand[q * a.trace_cap + n_exp] = u;
+                ++n_exp;
+                const int32_t* row = ix.ell + (int64_t)u * ELLW;
+                int32_t vv[ELLW / 32];
+#pragma unroll
+                for (int c = 0; c < ELLW / 32; ++c) vv[c] = __ldg(row + c * 32 + lane);
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < ELLW / 32; ++c) {
+                    if (status == 0) batch(vv[c]);
+                }
+                if (it >= kIterCap) status = 2;
+            }
+        }
+        // ---- outputs (a7 candidate list + top-k)
+        const float inf = __int_as_float(0x7f800000);
+        if (a.cand_ids) {
+            for (int i = lane; i < ef; i += 32) {
+                a.cand_ids[q * ef + i] = i < csz ? key_id(cur[i]) : -1;
+                a.cand_d[q * ef + i] = i < csz ? key_dist(cur[i]) : inf;
+            }
+        }
+        for (int i = lane; i < a.k; i += 32) {
+            a.out_ids[q * a.k + i] = i < csz ? key_id(cur[i]) : -1;
+            a.out_d[q * a.k + i] = i < csz ? key_dist(cur[i]) : inf;
+        }
+        if (lane == 0) {
+            if (a.counters) {
+                int4 c4 = make_int4(n_exp, n_dist, n_spill, status);
+                reinterpret_cast<int4*>(a.counters)[q] = c4;
+            }
+            if (TRACE) { a.trace_nexp[q] = n_exp; a.trace_nvis[q] = n_dist; }
+        }
+        __syncwarp();
+    }
+}
+
+template <int METRIC, int ELLW, bool TRACE>
+void* kernel_ptr() { return (void*)k_traverse<METRIC, ELLW, TRACE>; }
+
+void* pick(int metric, int ellw, bool trace) {
+    if (metric == 0) {
+        if (ellw == 32) return trace ? kernel_ptr<0, 32, true>() : kernel_ptr<0, 32, false>();
+        return trace ? kernel_ptr<0, 64, true>() : kernel_ptr<0, 64, false>();
+    }
+    if (ellw == 32) return trace ? kernel_ptr<1, 32, true>() : kernel_ptr<1, 32, false>();
+    return trace ? kernel_ptr<1, 64, true>() : kernel_ptr<1, 64, false>();
+}
+
+size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
+    size_t per_warp = (size_t)(2 * a.ef + 32) * 8 + (size_t)ix.rdim_pad * 4 + ((size_t)4 << a.hash_log2);
+    return per_warp * kTW;
+}
+}  // namespace
+
+int traverse_max_warps(const DevIndex& ix, const SearchArgs& a) {
+    void* fn = pick(ix.metric, ix.ell_w, a.trace_cap > 0);
+    size_t smem = smem_bytes(ix, a);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int blocks = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kTW * 32, smem);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks < 1) return 0;
+    return blocks * sms * kTW;
+}
+
+int launch_traverse(const DevIndex& ix, const SearchArgs& a, int grid_warps, cudaStream_t s) {
+    if (a.m == 0) return 0;
+    void* fn = pick(ix.metric, ix.ell_w, a.trace_cap > 0);
+    size_t smem = smem_bytes(ix, a);
+    int64_t want = (a.m + kTW - 1) / kTW;
+    int64_t blocks = grid_warps / kTW;
+    if (blocks > want) blocks = want;
+    if (blocks < 1) blocks = 1;
+    cudaMemsetAsync(a.work, 0, sizeof(int32_t), s);
+    SearchArgs aa = a;
+    DevIndex ii = ix;
+    void* args[] = {&ii, &aa};
+    cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(kTW * 32), args, smem, s);
+    return 1;
+}
+
+}  // namespace pa

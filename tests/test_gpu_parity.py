@@ -1,0 +1,174 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element
+on the same seeded inputs (tie-aware protocol in tests/parity.py)."""
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_2503_21206_b200 as pa
+from conftest import golden_names, instance_from_golden, load_golden
+from gpu_util import run_gpu
+from parity import compare
+from tiny import tiny_instance
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__ as g
+    g.build_library()
+
+
+def integer_instance(n=300, D=16, R=8, m=40, seed=5, r=4, metric="l2", member_ratio=0.6):
+    """All coordinates small integers and V a signed permutation: every fp32
+    operation of the GPU path is exact, so trajectories must be bit-exact
+    INCLUDING ties (many exact ties by construction)."""
+    rng = np.random.default_rng(seed)
+    inst = tiny_instance(n=n, D=D, dp=D // 2, R=R, m=m, seed=seed, r=r, metric=metric, member_ratio=member_ratio)
+    X = rng.integers(-4, 5, size=(n, D)).astype(np.float32)
+    perm = rng.permutation(D)
+    sign = np.where(rng.random(D) < 0.5, -1.0, 1.0)
+    V = np.zeros((D, D), np.float32)
+    V[perm, np.arange(D)] = sign
+    Xh = (X.astype(np.float64) @ V.astype(np.float64)).astype(np.float32)
+    inst["basis"], inst["rotated"] = V, Xh
+    inst["reduced"] = np.ascontiguousarray(Xh[:, :D // 2])
+    inst["queries"] = rng.integers(-4, 5, size=(m, D)).astype(np.float32)
+    pool = inst["fes_pool_ids"]
+    cuts = inst["fes_cell_off"]
+    inst["fes_centroids"] = np.stack([np.round(inst["reduced"][pool[cuts[c]:cuts[c + 1]]].mean(0))
+                                      for c in range(len(cuts) - 1)]).astype(np.float32)
+    return inst
+
+
+def _both(inst, k, ef, trace_cap=4096, **opts):
+    ix = pa.Index.from_instance(inst)
+    g = run_gpu(ix, inst, k, ef, trace_cap=trace_cap, **opts)
+    flags = opts.get("flags", 0)
+    r = orc.search(inst, k=k, ef=ef, stages=1, trace_cap=trace_cap, flags=flags,
+                   **{kk: v for kk, v in opts.items() if kk in ("entries", "ef1") and v})
+    ix.close()
+    return g, r
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_fixtures_bit_exact(name):
+    gd = load_golden(name)
+    inst = instance_from_golden(gd)
+    g, r = _both(inst, gd["k"], gd["ef"], entries=gd["entries"])
+    assert list(g["trace_expand"][0][:g["trace_nexp"][0]]) == gd["expand"]
+    assert list(g["trace_visit"][0][:g["trace_nvis"][0]]) == gd["visit"]
+    assert list(g["ids"][0]) == gd["result_ids"]
+    assert np.array_equal(g["d"][0], np.array(gd["result_d"], np.float32))
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_integer_fixture_bit_exact_with_ties(metric, seed):
+    inst = integer_instance(seed=seed, metric=metric)
+    for ef in (8, 32):
+        g, r = _both(inst, 5, ef)
+        rep = compare(inst, g, r, 5, ef)
+        assert not rep.fail, rep.fail[:3]
+        assert rep.tie == 0, rep                       # exact arithmetic: no divergence allowed
+        assert np.array_equal(g["ids"], r["ids"])
+        assert np.array_equal(g["d"].astype(np.float64), r["d"])
+        assert np.array_equal(g["cand_ids"], r["cand1_ids"])
+        assert np.array_equal(g["n_dist1"], r["n_dist1"]) and np.array_equal(g["n_exp1"], r["n_exp1"])
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_ef_ge_members_is_brute_force(metric):
+    inst = tiny_instance(n=400, D=24, dp=12, R=10, m=33, seed=7, metric=metric, member_ratio=0.5)
+    nm = int(inst["member_flags"].sum())
+    ef = min(256, nm)
+    assert nm <= 256
+    ix = pa.Index.from_instance(inst)
+    g = run_gpu(ix, inst, 10, ef, entries=8)
+    Qh = orc.project(inst["queries"], inst["basis"])
+    bi, bd = orc.brute_force(Qh, inst["reduced"], 10, metric=metric, ids=np.flatnonzero(inst["member_flags"]))
+    assert orc.recall(g["ids"], bi, 10, ret_d=g["d"].astype(np.float64), gt_d=bd) == 1.0
+    tol = 1e-5 * np.abs(bd) + 1e-6
+    assert np.all(np.abs(np.sort(g["d"], 1) - bd) <= tol)
+
+
+@pytest.mark.parametrize("cfg_name", ["C0", "S1", "S2"])
+def test_config_parity(cfg_name, request):
+    inst = request.getfixturevalue(cfg_name.lower())
+    cfg = inst["cfg"]
+    g, r = _both(inst, cfg.k, cfg.ef, trace_cap=8192)
+    rep = compare(inst, g, r, cfg.k, cfg.ef, gt_ids=inst["gt_sub_ids"][:, :cfg.k])
+    print(cfg_name, rep, getattr(rep, "recall_gpu", None), getattr(rep, "recall_orc", None))
+    assert not rep.fail, rep.fail[:5]
+    assert rep.exact >= 0.9 * cfg.m, rep
+    assert np.all(g["status"] == 0)
+
+
+def test_forced_spill_is_exact(s1):
+    cfg = s1["cfg"]
+    ix = pa.Index.from_instance(s1)
+    base = run_gpu(ix, s1, cfg.k, cfg.ef, trace_cap=8192)
+    for log2 in (5, 9):
+        sp = run_gpu(ix, s1, cfg.k, cfg.ef, trace_cap=8192, hash_slots_log2=log2)
+        assert sp["spill"].sum() > 0
+        for key in ("ids", "d", "cand_ids", "cand_dists", "trace_expand", "trace_visit", "n_dist1"):
+            assert np.array_equal(base[key], sp[key]), key
+    ix.close()
+
+
+def test_edge_cases(s1):
+    cfg = s1["cfg"]
+    ix = pa.Index.from_instance(s1)
+    one = s1["queries"][:1]
+    g1 = run_gpu(ix, s1, cfg.k, cfg.ef, queries=one)
+    r1 = orc.search(s1, queries=one, k=cfg.k, ef=cfg.ef)
+    assert orc.recall(g1["ids"], r1["ids"], cfg.k) >= 0.9
+    # ef = k = 1
+    g = run_gpu(ix, s1, 1, 1)
+    r = orc.search(s1, k=1, ef=1)
+    assert (g["ids"][:, 0] == r["ids"][:, 0]).mean() >= 0.9
+    # ef = 256 and E larger than every cell (entries = whole cell)
+    g = run_gpu(ix, s1, 10, 256, entries=1024)
+    assert np.all(g["status"] == 0) and np.all(g["ids"] >= 0)
+    # toggles
+    g = run_gpu(ix, s1, 10, 64, flags=pa.PA_NO_FES)
+    r = orc.search(s1, k=10, ef=64, flags=orc.NO_FES)
+    assert orc.recall(g["ids"], r["ids"], 10) >= 0.98
+    g = run_gpu(ix, s1, 10, 64, flags=pa.PA_NO_STAGE1)
+    r = orc.search(s1, k=10, ef=64, flags=orc.NO_STAGE1)
+    assert orc.recall(g["ids"], r["ids"], 10) >= 0.98
+    assert np.all(g["n_exp1"] == 0)
+    # m = 0 is a no-op
+    import torch
+    z = torch.empty(0, s1["D"], device="cuda")
+    ix.search_device(z, 10, 64, torch.empty(0, 10, dtype=torch.int32, device="cuda"),
+                     torch.empty(0, 10, device="cuda"))
+    with pytest.raises(pa.PAError):
+        run_gpu(ix, s1, 10, 5)                     # ef < k
+    with pytest.raises(pa.PAError):
+        run_gpu(ix, s1, 10, 300)                   # ef > 256
+    ix.close()
+
+
+def test_host_path_equals_device_path(s1):
+    cfg = s1["cfg"]
+    ix = pa.Index.from_instance(s1)
+    g = run_gpu(ix, s1, cfg.k, cfg.ef)
+    ids, d = ix.search(s1["queries"], k=cfg.k, ef=cfg.ef)
+    assert np.array_equal(ids, g["ids"]) and np.array_equal(d, g["d"])
+    ci, cd = ix.search_candidates(s1["queries"], ef=cfg.ef)
+    assert np.array_equal(ci, g["cand_ids"]) and np.array_equal(cd, g["cand_dists"])
+    st = ix.stats()
+    assert st["kernel_launches"] >= 3 and st["ms_total_gpu"] > 0
+    ix.close()
+    with pytest.raises(pa.PAError) as e:
+        ix2 = pa.Index.from_instance(s1)
+        h = ix2._h
+        ix2.close()
+        ix2._h = h                                 # use after destroy → PA_ESTATE
+        ix2.search(s1["queries"], k=10, ef=64)
+    assert e.value.status == pa.PA_ESTATE
+    ix2._h = None
