@@ -57,8 +57,8 @@ class Config:
     r: int = 32             # FES cells
     n_e: int = 65536        # FES pool cap (SURVEY §8.0 †)
     shape: str = "iid"      # "iid" | "mixture"
-    alpha: float = 0.8      # spectrum decay
-    sc: float = 2.0         # centre scale
+    alpha: float = 1.6      # spectrum decay (tuned, DESIGN.md §Input recipe)
+    sc: float = 1.0         # centre scale (tuned: clusters overlap → navigable kNN graph)
     ood_shift: float = 0.0  # IP query shift (T2I-shaped)
     seed: int = 2503
     gt_k: int = 100
@@ -75,21 +75,21 @@ CONFIGS = {
                  k=10, ef=64, shape="iid", seed=2503),
     # configs[1]: DEEP-shaped 10M x 96 L2, d'=48, 10K queries, 1 B200 (s=0.33 from Table 4 DEEP)
     "C1": Config("C1-DEEP-10M", N=10_000_000, D=96, dp=48, metric="l2", ratio=0.33, m=10_000,
-                 k=10, ef=64, shape="mixture", alpha=0.8, seed=2504),
+                 k=10, ef=64, shape="mixture", seed=2504),
     # configs[2]: T2I-shaped 100M x 200 IP, d'=64 (s=0.25)
     "C2": Config("C2-T2I-100M", N=100_000_000, D=200, dp=64, metric="ip", ratio=0.25, m=10_000,
-                 k=10, ef=64, shape="mixture", alpha=0.8, ood_shift=0.5, seed=2505),
+                 k=10, ef=64, shape="mixture", ood_shift=0.5, seed=2505),
     # configs[3]: LAION-shaped 100M x 768, d'=128 (s=0.25)
     "C3": Config("C3-LAION-100M", N=100_000_000, D=768, dp=128, metric="l2", ratio=0.25, m=10_000,
-                 k=10, ef=64, shape="mixture", alpha=1.0, seed=2506),
+                 k=10, ef=64, shape="mixture", seed=2506),
     # configs[4]: WIKI-shaped 100M x 768 sweep
     "C4": Config("C4-WIKI-100M", N=100_000_000, D=768, dp=128, metric="l2", ratio=0.25, m=65_536,
-                 k=10, ef=64, shape="mixture", alpha=1.0, seed=2507),
+                 k=10, ef=64, shape="mixture", seed=2507),
     # scaled-down shaped configs used by parity tests (same recipe, oracle-sized)
     "S1": Config("S1-DEEP-shaped-20K", N=20_000, D=96, dp=48, metric="l2", ratio=0.33, m=256,
-                 k=10, ef=64, shape="mixture", alpha=0.8, seed=2604),
+                 k=10, ef=64, shape="mixture", seed=2604),
     "S2": Config("S2-T2I-shaped-20K", N=20_000, D=200, dp=64, metric="ip", ratio=0.25, m=256,
-                 k=10, ef=64, shape="mixture", alpha=0.8, ood_shift=0.5, seed=2605),
+                 k=10, ef=64, shape="mixture", ood_shift=0.5, seed=2605),
 }
 
 
@@ -214,7 +214,7 @@ def csr_from_rows(rows: np.ndarray, N: int, ids: Optional[np.ndarray] = None):
 
 
 def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, labels=None,
-              metric: str = "l2", P: int = 5, chunk: int = 4096):
+              metric: str = "l2", P: int = 0, chunk: int = 4096, refine: int = int(__import__("os").environ.get("PA_KNN_REFINE", "0"))):
     """Degree-R kNN graph over the rows `ids` of X (all rows if None), neighbour
     lists in ascending-distance order, self excluded.  Exact brute force when
     `labels` is None; otherwise candidates are restricted to the P nearest
@@ -240,6 +240,7 @@ def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, label
         return out
     lab = labels[ids]
     Kc = int(labels.max().item()) + 1
+    P = P or int(__import__("os").environ.get("PA_KNN_P", "8"))
     order = torch.argsort(lab, stable=True)
     counts = torch.bincount(lab, minlength=Kc)
     starts = torch.zeros(Kc + 1, dtype=torch.int64, device=dev)
@@ -268,7 +269,61 @@ def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, label
         v, jj = torch.topk(d, kk, dim=1, largest=False)
         g = torch.where(torch.isfinite(v), ids[cand[jj]], torch.full_like(jj, -1))
         out[a, :kk] = g
+    if refine:
+        out = refine_knn(X, out, ids, iters=refine)
     return out
+
+
+def partition_labels(X: torch.Tensor, K: int, seed: int, iters: int = 8, sample: int = 1 << 20,
+                     chunk: int = 1 << 18) -> torch.Tensor:
+    """Geometric partition for kNN candidate generation (graph tool only):
+    k-means (random init, `iters` Lloyd steps on a ≤`sample`-row sample), then
+    every row is assigned to its nearest centre.  → int64 labels [N]."""
+    N = X.shape[0]
+    dev = X.device
+    rng = np.random.Generator(np.random.Philox(key=seed + 11))
+    sidx = torch.from_numpy(np.sort(rng.choice(N, size=min(N, sample), replace=False))).to(dev)
+    S = X[sidx]
+    C = S[torch.from_numpy(rng.choice(S.shape[0], size=K, replace=False)).to(dev)].clone()
+    for _ in range(iters):
+        a = torch.cat([torch.argmin(_sqdist(S[s:s + chunk], C), 1) for s in range(0, S.shape[0], chunk)])
+        cnt = torch.bincount(a, minlength=K).float()
+        newC = torch.zeros_like(C).index_add_(0, a, S)
+        keep = cnt > 0
+        C[keep] = newC[keep] / cnt[keep, None]
+    return torch.cat([torch.argmin(_sqdist(X[s:s + chunk], C), 1) for s in range(0, N, chunk)])
+
+
+def refine_knn(X: torch.Tensor, rows: torch.Tensor, ids: torch.Tensor, iters: int = 2, chunk: int = 2048):
+    """Neighbour-of-neighbour refinement of an approximate kNN graph (NN-descent
+    style join; graph tool only).  rows [n][R] global ids (−1 padded) aligned with
+    `ids`; each pass replaces a row by the R nearest of (row ∪ rows of its row)."""
+    dev = X.device
+    n, R = rows.shape
+    N = X.shape[0]
+    pos = torch.full((N,), -1, dtype=torch.int64, device=dev)
+    pos[ids] = torch.arange(n, device=dev)
+    for _ in range(iters):
+        new = torch.empty_like(rows)
+        for s in range(0, n, chunk):
+            e = min(n, s + chunk)
+            r0 = rows[s:e]                                           # [B][R]
+            p0 = pos[r0.clamp_min(0)]
+            two = rows[p0.clamp_min(0)]                              # [B][R][R]
+            two = torch.where((r0 >= 0)[:, :, None] & (p0 >= 0)[:, :, None], two, torch.full_like(two, -1))
+            cand = torch.cat([r0, two.reshape(e - s, R * R)], 1)
+            cand, _ = torch.sort(cand, 1)
+            dup = torch.zeros_like(cand, dtype=torch.bool)
+            dup[:, 1:] = cand[:, 1:] == cand[:, :-1]
+            me = ids[s:e][:, None]
+            bad = dup | (cand < 0) | (cand == me)
+            x = X[cand.clamp_min(0)]                                 # [B][C][D]
+            d = ((x - X[ids[s:e]][:, None, :]) ** 2).sum(2)
+            d = torch.where(bad, torch.full_like(d, float("inf")), d)
+            v, j = torch.topk(d, R, dim=1, largest=False)
+            new[s:e] = torch.where(torch.isfinite(v), torch.gather(cand, 1, j), torch.full_like(j, -1))
+        rows = new
+    return rows
 
 
 def sample_members(offsets: np.ndarray, nbrs: np.ndarray, ratio: float, seed: int) -> np.ndarray:
@@ -455,7 +510,9 @@ def build_instance(cfg: Config, device="cpu", with_full_graph: bool = True, gt: 
     as host numpy arrays, plus ground truths for recall.  Deterministic per cfg."""
     X, labels = gen_base(cfg, device)
     Q = gen_queries(cfg, device)
-    lab = labels if cfg.shape == "mixture" else None
+    lab = None                       # ≤ 50K rows: exact brute-force kNN
+    if cfg.N > 50_000:               # larger: cluster-local kNN + neighbour-of-neighbour refinement
+        lab = labels if labels is not None else partition_labels(X, max(1, cfg.N // 1000), cfg.seeds["graph"])
     full_rows = knn_graph(X, cfg.R, labels=lab, metric="l2")
     full_off, full_nbrs = csr_from_rows(full_rows.cpu().numpy(), cfg.N)
     del full_rows

@@ -150,7 +150,7 @@ pa_status pa_search(pa_index* ix, const float* queries, int64_t m, int32_t k, in
                     const pa_search_opts* opts, int32_t* out_ids, float* out_dists);
 
 /* GPU stage only, all arrays DEVICE-resident on the index's device, enqueued on
- * `stream` (a cudaStream_t; NULL = the index's own stream) and NOT
+ * `stream` (a cudaStream_t; NULL = the legacy default stream) and NOT
  * synchronised: q [m][dim] → out_ids/out_dists [m][k] (reduced δ'), plus the
  * optional debug outputs.  This is the call bench.py times with inputs already
  * resident in HBM. */

@@ -488,7 +488,7 @@ pa_status pa_search_device(pa_index* ix, const float* d_queries, int64_t m, int3
     if (r.stages != PA_STAGES_GPU) return fail(PA_EINVAL, "pa_search_device runs stage 1 only");
     std::lock_guard<std::mutex> g(ix->mu);
     CU(cudaSetDevice(ix->device));
-    cudaStream_t s = stream ? (cudaStream_t)stream : ix->stream;
+    cudaStream_t s = (cudaStream_t)stream;          // NULL = the legacy default stream (CUDA convention)
     if (m == 0) return PA_OK;
     return enqueue_gpu_stage(ix, d_queries, m, k, r, d_out_ids, d_out_dists, dbg, false, s);
 }

@@ -143,7 +143,7 @@ def compare(inst, gpu: dict, ref: dict, k: int, ef: int, gt_ids=None, check_trac
                 if v not in vis_set:
                     vis_set.add(int(v))
                     nvis_prefix += 1
-        if not np.array_equal(vg[:nvis_prefix], vo[:nvis_prefix]):
+        if not np.array_equal(vg[nE:nvis_prefix], vo[nE:nvis_prefix]):
             rep.fail.append((q, f"visit prefix differs before expansion step {t}"))
             continue
         vis = np.array(sorted(vis_set), np.int64)
