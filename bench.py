@@ -93,11 +93,18 @@ def measured_peaks():
 
 
 # --------------------------------------------------------------- instance --
-def make_instance(cfg_name, world, rank, m_per_rank):
+def make_instance(cfg_name, world, rank, m_per_rank, cache=None):
     import torch
     import datagen as dg
     cfg = dg.get_config(cfg_name, m=m_per_rank * world)
     t0 = time.time()
+    path = os.path.join(cache, f"inst_{cfg_name}_{world}_{rank}_{m_per_rank}.npz") if cache else None
+    if path and os.path.exists(path):
+        z = np.load(path, allow_pickle=False)
+        inst = {k: z[k] for k in z.files}
+        inst["cfg"], inst["metric"] = cfg, cfg.metric
+        log(f"[rank {rank}] instance loaded from {path} in {time.time() - t0:.1f}s")
+        return cfg, inst
     inst = dg.build_instance(cfg, device=f"cuda:{torch.cuda.current_device()}", gt=False)
     Q = inst["queries"]
     lo, hi = rank * m_per_rank, (rank + 1) * m_per_rank
@@ -115,6 +122,9 @@ def make_instance(cfg_name, world, rank, m_per_rank):
     torch.cuda.empty_cache()
     log(f"[rank {rank}] instance {cfg.name}: N={cfg.N} D={cfg.D} d'={cfg.dp} members={int(inst['member_flags'].sum())}"
         f" m={m_per_rank} built in {time.time() - t0:.1f}s")
+    if path:
+        os.makedirs(cache, exist_ok=True)
+        np.savez(path, **{k: v for k, v in inst.items() if isinstance(v, np.ndarray)})
     return cfg, inst
 
 
@@ -178,7 +188,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    cfg, inst = make_instance(args.config, world, rank, args.m)
+    cfg, inst = make_instance(args.config, world, rank, args.m, args.cache)
     k = cfg.k
     m = inst["queries"].shape[0]
     t0 = time.time()
@@ -364,6 +374,7 @@ def main():
     ap.add_argument("--full-sweep", action="store_true")
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cache", default=None, help="dir to cache the generated instance (same-call reuse only)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

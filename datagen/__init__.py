@@ -240,7 +240,7 @@ def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, label
         return out
     lab = labels[ids]
     Kc = int(labels.max().item()) + 1
-    P = P or int(__import__("os").environ.get("PA_KNN_P", "8"))
+    P = P or int(__import__("os").environ.get("PA_KNN_P", "32"))
     order = torch.argsort(lab, stable=True)
     counts = torch.bincount(lab, minlength=Kc)
     starts = torch.zeros(Kc + 1, dtype=torch.int64, device=dev)
@@ -512,7 +512,8 @@ def build_instance(cfg: Config, device="cpu", with_full_graph: bool = True, gt: 
     Q = gen_queries(cfg, device)
     lab = None                       # ≤ 50K rows: exact brute-force kNN
     if cfg.N > 50_000:               # larger: cluster-local kNN + neighbour-of-neighbour refinement
-        lab = labels if labels is not None else partition_labels(X, max(1, cfg.N // 1000), cfg.seeds["graph"])
+        use_gen = __import__("os").environ.get("PA_KNN_LABELS", "geo") == "gen" and labels is not None
+        lab = labels if use_gen else partition_labels(X, max(1, cfg.N // 1000), cfg.seeds["graph"])
     full_rows = knn_graph(X, cfg.R, labels=lab, metric="l2")
     full_off, full_nbrs = csr_from_rows(full_rows.cpu().numpy(), cfg.N)
     del full_rows

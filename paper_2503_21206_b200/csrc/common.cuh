@@ -83,6 +83,57 @@ __device__ __forceinline__ int warp_merge(const uint64_t* A, int csz, uint64_t x
     return ns < cap ? ns : cap;
 }
 
+// In-place rank merge of the passing lanes' keys (ballot `pb` ≠ 0) into the
+// sorted smem list C[0..csz) with capacity cap ≤ 32·SMAX; returns the new size
+// and (minr) the smallest position a new key landed at.  For every passing key x
+// the warp counts with ef/32 ballots rank_C(x) = #{C < x} and, per C entry, the
+// number of passing keys below it (its right shift); keys are unique so the
+// final positions rank_C(x) + #{passing < x} and i + shift(i) are a permutation.
+template <int SMAX>
+__device__ __forceinline__ int rank_merge(uint64_t* C, int csz, int cap, uint64_t key, bool pass, unsigned pb,
+                                          int lane, int& minr) {
+    uint64_t c[SMAX];
+    int sh[SMAX];
+#pragma unroll
+    for (int t = 0; t < SMAX; ++t) {
+        const int i = lane + 32 * t;
+        c[t] = i < csz ? C[i] : kKeyInf;
+        sh[t] = 0;
+    }
+    const int np = __popc(pb);
+    int rc = 0, rn = 0;
+    minr = cap;
+    while (pb) {
+        const int src = __ffs(pb) - 1;
+        pb &= pb - 1;
+        const uint64_t x = ((uint64_t)__shfl_sync(kFull, (uint32_t)(key >> 32), src) << 32) |
+                           __shfl_sync(kFull, (uint32_t)key, src);
+        int r = 0;
+#pragma unroll
+        for (int t = 0; t < SMAX; ++t) {
+            const bool lt = c[t] < x;
+            sh[t] += lt ? 0 : 1;
+            r += __popc(__ballot_sync(kFull, lt));
+        }
+        if (lane == src) rc = r;
+        minr = min(minr, r);
+        rn += (x < key) ? 1 : 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < SMAX; ++t) {
+        const int i = lane + 32 * t;
+        const int pos = i + sh[t];
+        if (i < csz && pos < cap) C[pos] = c[t];
+    }
+    if (pass) {
+        const int pos = rc + rn;
+        if (pos < cap) C[pos] = key;
+    }
+    __syncwarp();
+    return min(csz + np, cap);
+}
+
 // Direct-form distance (Alg 1 l.8) between an smem query row and a global row
 // of `dps` floats (multiple of 4, 16-B aligned): L2 = Σ(x−q)², IP = −Σ x·q.
 // Four independent fp32 FMA chains over float4 slices (Q24: fp32, RNE, FMA).

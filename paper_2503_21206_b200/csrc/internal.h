@@ -20,6 +20,8 @@ struct DevIndex {
     int32_t* cell_off = nullptr;               // [r+1]
     int32_t* pool_ids = nullptr;               // [pool_n] grouped by cell
     float* pool_vec = nullptr;                 // [pool_n][rdim_pad] contiguous by cell
+    float* proj_bt = nullptr;                  // [roundup16(r + dim)][dim] B_T of the tcgen05 projection
+    float* cent_norm = nullptr;                // [r] ‖centroid‖²
 };
 
 struct SearchArgs {
@@ -31,6 +33,7 @@ struct SearchArgs {
     float* qp = nullptr;           // [m][rdim_pad]  projected q'
     float* qres = nullptr;         // [m][dim − rdim] (optional) residual projection for host stages
     int32_t* cell = nullptr;       // [m]
+    bool cell_ready = false;       // routing already computed (by the tcgen05 projection epilogue)
     int32_t* entries = nullptr;    // [m][E]
     int32_t* cand_ids = nullptr;   // [m][ef] (optional)
     float* cand_d = nullptr;       // [m][ef] (optional)
@@ -52,6 +55,8 @@ struct SearchArgs {
 
 // kernels (each returns the number of kernel launches it enqueued)
 int launch_project(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
+int launch_project_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
+bool project_tc_supported(const DevIndex& ix, bool with_qres);
 int launch_fes(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
 int launch_traverse(const DevIndex& ix, const SearchArgs& a, int grid_warps, cudaStream_t s);
 int traverse_max_warps(const DevIndex& ix, const SearchArgs& a);   // resident warps for the launch config

@@ -100,7 +100,13 @@ pa_status check_csr(const int64_t* off, const int32_t* nb, int64_t n, int32_t ma
     return PA_OK;
 }
 
-int default_hash_log2(int ef) { return ef <= 64 ? 12 : 13; }
+int default_hash_log2(int ef) {
+    if (const char* e = std::getenv("PA_HASH_LOG2")) {
+        int v = std::atoi(e);
+        if (v >= 5 && v <= 15) return v;
+    }
+    return ef <= 64 ? 11 : 12;
+}
 
 }  // namespace
 
@@ -252,7 +258,13 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
 
     int launches = 0;
     CU(cudaEventRecord(ix->ev[0], s));
-    launches += pa::launch_project(ix->dev, a, s);
+    static const bool force_simt = [] { const char* e = std::getenv("PA_PROJECT"); return e && !std::strcmp(e, "simt"); }();
+    if (!force_simt && pa::project_tc_supported(ix->dev, a.qres != nullptr)) {
+        launches += pa::launch_project_tc(ix->dev, a, s);
+        a.cell_ready = true;
+    } else {
+        launches += pa::launch_project(ix->dev, a, s);
+    }
     CU(cudaGetLastError());
     CU(cudaEventRecord(ix->ev[1], s));
     launches += pa::launch_fes(ix->dev, a, s);
@@ -453,6 +465,29 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
         CUB(dalloc(&d.pool_vec, pv.size()));
         CUB(cudaMemcpy(d.pool_vec, pv.data(), sizeof(float) * pv.size(), cudaMemcpyHostToDevice));
     }
+    // tcgen05 projection operand B_T = [(V_{:d'}·Cᵀ)ᵀ ; Vᵀ] (rows K-major), fp64 → fp32, zero-padded
+    {
+        const int rows = ((r + D) + 15) & ~15;
+        std::vector<float> bt((size_t)rows * D, 0.f);
+        for (int c = 0; c < r; ++c)
+            for (int k = 0; k < D; ++k) {
+                double s = 0;
+                for (int j = 0; j < dp; ++j) s += (double)p->basis[(size_t)k * D + j] * (double)p->fes_centroids[(size_t)c * dp + j];
+                bt[(size_t)c * D + k] = (float)s;
+            }
+        for (int j = 0; j < D; ++j)
+            for (int k = 0; k < D; ++k) bt[(size_t)(r + j) * D + k] = p->basis[(size_t)k * D + j];
+        std::vector<float> cn(r);
+        for (int c = 0; c < r; ++c) {
+            double s = 0;
+            for (int j = 0; j < dp; ++j) s += (double)p->fes_centroids[(size_t)c * dp + j] * p->fes_centroids[(size_t)c * dp + j];
+            cn[c] = (float)s;
+        }
+        CUB(dalloc(&d.proj_bt, bt.size()));
+        CUB(cudaMemcpy(d.proj_bt, bt.data(), sizeof(float) * bt.size(), cudaMemcpyHostToDevice));
+        CUB(dalloc(&d.cent_norm, cn.size()));
+        CUB(cudaMemcpy(d.cent_norm, cn.data(), sizeof(float) * cn.size(), cudaMemcpyHostToDevice));
+    }
     ix->h_sub_off.assign(p->sub_offsets, p->sub_offsets + n + 1);
     ix->h_sub_nb.assign(p->sub_neighbors, p->sub_neighbors + p->sub_offsets[n]);
     CUB(cudaDeviceSynchronize());
@@ -613,7 +648,7 @@ void pa_destroy(pa_index* ix) {
     cudaFreeHost(ix->h_counters);
     auto& d = ix->dev;
     cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
-    cudaFree(d.pool_ids); cudaFree(d.pool_vec);
+    cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
     if (ix->stream) cudaStreamDestroy(ix->stream);
     ix->magic = 0;

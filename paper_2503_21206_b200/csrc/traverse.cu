@@ -3,18 +3,22 @@
 // global work counter.
 //
 // Per query (warp):
-//   C        : sorted list of ≤ ef 64-bit keys (ord(δ)<<32 | id<<1 | checked) in smem,
-//              ping-pong buffers A/B, merged by rank (common.cuh warp_merge).
-//   visited  : EXACT set (needed for Alg 1's "unvisited" test to be bit-faithful,
-//              I4) — level 1 = open-addressing int32 hash in smem (2^hash_log2
-//              slots, accepts inserts while ≤ half full); level 2 = per-warp
-//              epoch-tagged 64-bit hash slab in global memory once level 1 closes.
-//              The paper's bloom filter is NEXT-f1.
-//   loop     : u ← smallest unchecked key (warp ballot over C, Alg 1 l.5);
+//   C        : sorted list of ≤ ef 64-bit keys (ord(δ)<<32 | id<<1 | checked) in
+//              smem; lane l owns positions l, l+32, ... during a merge.
+//   visited  : EXACT set (Alg 1's "unvisited" test, I4) — level 1 = open-addressing
+//              int32 hash in smem (2^hash_log2 slots, accepts inserts while ≤ half
+//              full); level 2 = per-warp epoch-tagged 64-bit hash slab in global
+//              memory once level 1 closes.  The paper's bloom filter
+//              is NEXT-f1.
+//   loop     : u ← smallest unchecked key (ballot scan from a "all checked before"
+//              hint, Alg 1 l.5); the runner-up's ELL row is prefetched into L2;
 //              ELL[u][lane] (one coalesced 128-B row per 32 neighbours, l.6);
-//              test-and-insert visited (l.7); new lanes gather their reduced row
-//              (float4 loads) and compute δ' in fp32 (l.8); warp bitonic sort of
-//              the ≤32 new keys and rank-merge into C truncated to ef (l.9, l.11).
+//              test-and-insert visited (l.7); each new neighbour's lane gathers its
+//              reduced row (float4 loads) and computes δ' in fp32 (l.8); keys
+//              below C's current worst are merged by rank (l.9, l.11): for every
+//              passing key the warp counts, with one shuffle and ef/32 ballots,
+//              its rank in C and its shift of C's entries; everything moves in
+//              place (registers hold the old C across one __syncwarp).
 #include "common.cuh"
 #include "internal.h"
 
@@ -73,17 +77,20 @@ __device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& 
     return false;   // unreachable while count2 ≤ gmask/2 (guarded by the caller)
 }
 
-template <int METRIC, int ELLW, bool TRACE>
-__global__ void __launch_bounds__(kTW * 32) k_traverse(DevIndex ix, SearchArgs a) {
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+}
+
+template <int METRIC, int ELLW, int SMAX, bool TRACE>
+__global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
-    const size_t per_warp = (size_t)(2 * ef + 32) * 8 + (size_t)dps * 4 + (size_t)S * 4;
+    const int efp = (ef + 1) & ~1;                      // keep qs 16-B aligned
+    const size_t per_warp = (size_t)efp * 8 + (size_t)dps * 4 + (size_t)S * 4;
     unsigned char* base = smem_raw + per_warp * w;
-    uint64_t* A0 = reinterpret_cast<uint64_t*>(base);
-    uint64_t* B0 = A0 + ef;
-    uint64_t* N = B0 + ef;
-    float* qs = reinterpret_cast<float*>(N + 32);
+    uint64_t* C = reinterpret_cast<uint64_t*>(base);
+    float* qs = reinterpret_cast<float*>(C + efp);
     int32_t* H = reinterpret_cast<int32_t*>(qs + dps);
     const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t gw = (int64_t)blockIdx.x * kTW + w;
@@ -108,12 +115,10 @@ __global__ void __launch_bounds__(kTW * 32) k_traverse(DevIndex ix, SearchArgs a
         for (int i = lane; i < (S >> 2); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
         __syncwarp();
 
-        uint64_t* cur = A0;
-        uint64_t* nxt = B0;
-        int csz = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
+        int csz = 0, hint = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
 
-        // Process one batch of ≤32 candidate ids (one per lane, −1 = none):
-        // visited test-and-insert, δ for new ids, sort, merge into C.
+        // One batch of ≤32 candidate ids (one per lane, −1 = none): visited
+        // test-and-insert, δ' for new ids, rank-merge of the keys that beat C's worst.
         auto batch = [&](int32_t v) {
             const bool open1 = vs.count1 + 32 <= cap1;
             if (!open1 && vs.count2 + 32 > cap2) { status = 1; return; }
@@ -132,14 +137,13 @@ __global__ void __launch_bounds__(kTW * 32) k_traverse(DevIndex ix, SearchArgs a
             if (nnew == 0) return;
             uint64_t key = kKeyInf;
             if (isnew) key = make_key(row_dist<METRIC>(qs, ix.reduced + (int64_t)v * dps, dps), v);
-            key = warp_sort32(key, lane);
-            if (csz == ef) {                       // nothing can enter C: skip the merge
-                uint64_t k0 = ((uint64_t)__shfl_sync(kFull, (uint32_t)(key >> 32), 0) << 32) |
-                              __shfl_sync(kFull, (uint32_t)key, 0);
-                if (k0 > cur[ef - 1]) return;
-            }
-            csz = warp_merge(cur, csz, key, nnew, nxt, N, ef, lane);
-            uint64_t* t = cur; cur = nxt; nxt = t;
+            const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
+            const bool pass = key < thresh;                   // unique keys: strict
+            unsigned pb = __ballot_sync(kFull, pass);
+            if (pb == 0) return;
+            int minr;
+            csz = rank_merge<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
+            hint = min(hint, minr);
         };
 
         // ---- a5: C := entries (Alg 1 l.3), visited := entries (Q15)
@@ -150,24 +154,31 @@ __global__ void __launch_bounds__(kTW * 32) k_traverse(DevIndex ix, SearchArgs a
         // ---- a6: Alg 1 l.4-12
         if (!(a.flags & 4u)) {
             for (int it = 0; status == 0; ++it) {
-                int p = -1;
-                for (int t = 0; t * 32 < csz; ++t) {
-                    int i = t * 32 + lane;
-                    bool un = i < csz && !key_checked(cur[i]);
-                    unsigned b = __ballot_sync(kFull, un);
-                    if (b) { p = t * 32 + __ffs(b) - 1; break; }
+                int p = -1, p2 = -1;
+                for (int t = hint >> 5; t * 32 < csz; ++t) {
+                    const int i = t * 32 + lane;
+                    const bool un = i < csz && !key_checked(C[i]);
+                    const unsigned b = __ballot_sync(kFull, un);
+                    if (b) {
+                        p = t * 32 + __ffs(b) - 1;
+                        const unsigned b2 = b & (b - 1);
+                        if (b2) p2 = t * 32 + __ffs(b2) - 1;
+                        break;
+                    }
                 }
                 if (p < 0) break;                                   // l.12: no unchecked node
-                const uint64_t ku = cur[p];
+                const uint64_t ku = C[p];
                 const int32_t u = key_id(ku);
-                __syncwarp();
-                if (lane == 0) cur[p] = ku | 1ull;                  // mark checked
-                if (TRACE && lane == 0 && n_exp < a.trace_cap) a.trace_expand[q * a.trace_cap + n_exp] = u;
-                ++n_exp;
                 const int32_t* row = ix.ell + (int64_t)u * ELLW;
                 int32_t vv[ELLW / 32];
 #pragma unroll
                 for (int c = 0; c < ELLW / 32; ++c) vv[c] = __ldg(row + c * 32 + lane);
+                if (p2 >= 0 && lane == 0) prefetch_l2(ix.ell + (int64_t)key_id(C[p2]) * ELLW);
+                __syncwarp();
+                if (lane == 0) C[p] = ku | 1ull;                    // mark checked
+                hint = p + 1;
+                if (TRACE && lane == 0 && n_exp < a.trace_cap) a.trace_expand[q * a.trace_cap + n_exp] = u;
+                ++n_exp;
                 __syncwarp();
 #pragma unroll
                 for (int c = 0; c < ELLW / 32; ++c) {
@@ -180,13 +191,13 @@ __global__ void __launch_bounds__(kTW * 32) k_traverse(DevIndex ix, SearchArgs a
         const float inf = __int_as_float(0x7f800000);
         if (a.cand_ids) {
             for (int i = lane; i < ef; i += 32) {
-                a.cand_ids[q * ef + i] = i < csz ? key_id(cur[i]) : -1;
-                a.cand_d[q * ef + i] = i < csz ? key_dist(cur[i]) : inf;
+                a.cand_ids[q * ef + i] = i < csz ? key_id(C[i]) : -1;
+                a.cand_d[q * ef + i] = i < csz ? key_dist(C[i]) : inf;
             }
         }
         for (int i = lane; i < a.k; i += 32) {
-            a.out_ids[q * a.k + i] = i < csz ? key_id(cur[i]) : -1;
-            a.out_d[q * a.k + i] = i < csz ? key_dist(cur[i]) : inf;
+            a.out_ids[q * a.k + i] = i < csz ? key_id(C[i]) : -1;
+            a.out_d[q * a.k + i] = i < csz ? key_dist(C[i]) : inf;
         }
         if (lane == 0) {
             if (a.counters) {
@@ -199,26 +210,30 @@ __global__ void __launch_bounds__(kTW * 32) k_traverse(DevIndex ix, SearchArgs a
     }
 }
 
-template <int METRIC, int ELLW, bool TRACE>
-void* kernel_ptr() { return (void*)k_traverse<METRIC, ELLW, TRACE>; }
-
-void* pick(int metric, int ellw, bool trace) {
-    if (metric == 0) {
-        if (ellw == 32) return trace ? kernel_ptr<0, 32, true>() : kernel_ptr<0, 32, false>();
-        return trace ? kernel_ptr<0, 64, true>() : kernel_ptr<0, 64, false>();
-    }
-    if (ellw == 32) return trace ? kernel_ptr<1, 32, true>() : kernel_ptr<1, 32, false>();
-    return trace ? kernel_ptr<1, 64, true>() : kernel_ptr<1, 64, false>();
+template <int METRIC, int ELLW, int SMAX>
+void* pick3(bool trace) {
+    return trace ? (void*)k_traverse<METRIC, ELLW, SMAX, true> : (void*)k_traverse<METRIC, ELLW, SMAX, false>;
+}
+template <int METRIC, int ELLW>
+void* pick2(int ef, bool trace) {
+    if (ef <= 64) return pick3<METRIC, ELLW, 2>(trace);
+    if (ef <= 128) return pick3<METRIC, ELLW, 4>(trace);
+    return pick3<METRIC, ELLW, 8>(trace);
+}
+void* pick(int metric, int ellw, int ef, bool trace) {
+    if (metric == 0) return ellw == 32 ? pick2<0, 32>(ef, trace) : pick2<0, 64>(ef, trace);
+    return ellw == 32 ? pick2<1, 32>(ef, trace) : pick2<1, 64>(ef, trace);
 }
 
 size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
-    size_t per_warp = (size_t)(2 * a.ef + 32) * 8 + (size_t)ix.rdim_pad * 4 + ((size_t)4 << a.hash_log2);
+    const size_t efp = (size_t)((a.ef + 1) & ~1);
+    size_t per_warp = efp * 8 + (size_t)ix.rdim_pad * 4 + ((size_t)4 << a.hash_log2);
     return per_warp * kTW;
 }
 }  // namespace
 
 int traverse_max_warps(const DevIndex& ix, const SearchArgs& a) {
-    void* fn = pick(ix.metric, ix.ell_w, a.trace_cap > 0);
+    void* fn = pick(ix.metric, ix.ell_w, a.ef, a.trace_cap > 0);
     size_t smem = smem_bytes(ix, a);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = 0, dev = 0, sms = 0;
@@ -231,7 +246,7 @@ int traverse_max_warps(const DevIndex& ix, const SearchArgs& a) {
 
 int launch_traverse(const DevIndex& ix, const SearchArgs& a, int grid_warps, cudaStream_t s) {
     if (a.m == 0) return 0;
-    void* fn = pick(ix.metric, ix.ell_w, a.trace_cap > 0);
+    void* fn = pick(ix.metric, ix.ell_w, a.ef, a.trace_cap > 0);
     size_t smem = smem_bytes(ix, a);
     int64_t want = (a.m + kTW - 1) / kTW;
     int64_t blocks = grid_warps / kTW;
