@@ -274,6 +274,20 @@ def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, label
     return out
 
 
+def build_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, labels=None):
+    """The graph tool used for both the full graph and the subgraph reconnect
+    ("same graph construction algorithm"): kNN candidates (L = 2R) →
+    occlusion pruning to R → reverse-edge fill.  PA_GRAPH=knn gives plain kNN."""
+    import os
+    if ids is None:
+        ids = torch.arange(X.shape[0], device=X.device)
+    if os.environ.get("PA_GRAPH", "rng") == "knn":
+        return knn_graph(X, R, ids=ids, labels=labels)
+    cand = knn_graph(X, 2 * R, ids=ids, labels=labels)
+    rows = prune_rng(X, ids, cand, R, alpha=float(os.environ.get("PA_GRAPH_ALPHA", "1.0")))
+    return reverse_fill(rows, ids, X, R)
+
+
 def partition_labels(X: torch.Tensor, K: int, seed: int, iters: int = 8, sample: int = 1 << 20,
                      chunk: int = 1 << 18) -> torch.Tensor:
     """Geometric partition for kNN candidate generation (graph tool only):
@@ -326,6 +340,80 @@ def refine_knn(X: torch.Tensor, rows: torch.Tensor, ids: torch.Tensor, iters: in
     return rows
 
 
+def prune_rng(X: torch.Tensor, ids: torch.Tensor, cand: torch.Tensor, R: int, alpha: float = 1.0,
+              chunk: int = 8192) -> torch.Tensor:
+    """Occlusion (RNG) pruning of distance-sorted candidate lists, the HNSW/Vamana
+    neighbour-selection heuristic ("occlusion rule"): candidate c is dropped
+    if an already kept s has alpha·δ(s, c) < δ(u, c).  → rows [n][R] (−1 padded)."""
+    dev = X.device
+    n, L = cand.shape
+    out = torch.full((n, R), -1, dtype=torch.int64, device=dev)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        c = cand[s:e]
+        valid = c >= 0
+        V = X[c.clamp_min(0)]                                    # [B][L][D]
+        u = X[ids[s:e]]
+        du = ((V - u[:, None, :]) ** 2).sum(2)                   # [B][L]
+        nv = (V * V).sum(2)
+        G = (nv[:, :, None] + nv[:, None, :] - 2.0 * torch.bmm(V, V.transpose(1, 2))).clamp_min_(0)
+        keep = torch.zeros_like(valid)
+        cnt = torch.zeros(e - s, dtype=torch.int64, device=dev)
+        for j in range(L):
+            occl = (keep & (alpha * G[:, :, j] < du[:, j:j + 1])).any(1)
+            take = valid[:, j] & ~occl & (cnt < R)
+            keep[:, j] = take
+            cnt += take.long()
+        # kept ids in candidate order, left-packed
+        order = torch.argsort((~keep).to(torch.int8), dim=1, stable=True)[:, :R]
+        kept = torch.gather(c, 1, order)
+        kk = torch.gather(keep, 1, order)
+        out[s:e, :kept.shape[1]] = torch.where(kk, kept, torch.full_like(kept, -1))
+    return out
+
+
+def reverse_fill(rows: torch.Tensor, ids: torch.Tensor, X: torch.Tensor, R: int) -> torch.Tensor:
+    """Fill the free slots of each row with reverse edges (u→v kept ⇒ v gets u),
+    nearest first, skipping ids already present (HNSW-style back-links)."""
+    dev = rows.device
+    n, W = rows.shape
+    N = X.shape[0]
+    pos = torch.full((N,), -1, dtype=torch.int64, device=dev)
+    pos[ids] = torch.arange(n, device=dev)
+    src = ids[:, None].expand(n, W).reshape(-1)
+    dst = rows.reshape(-1)
+    ok = dst >= 0
+    src, dst = src[ok], dst[ok]
+    dpos = pos[dst]
+    ok = dpos >= 0
+    src, dpos = src[ok], dpos[ok]
+    d = torch.empty(src.numel(), dtype=torch.float32, device=dev)
+    step = 1 << 22
+    for a0 in range(0, src.numel(), step):
+        a1 = min(src.numel(), a0 + step)
+        d[a0:a1] = ((X[src[a0:a1]] - X[ids[dpos[a0:a1]]]) ** 2).sum(1)
+    # sort by (target row, distance)
+    o = torch.argsort(d)
+    src, dpos, d = src[o], dpos[o], d[o]
+    o = torch.argsort(dpos, stable=True)
+    src, dpos = src[o], dpos[o]
+    out = torch.full((n, R), -1, dtype=torch.int64, device=dev)
+    out[:, :min(W, R)] = rows[:, :min(W, R)]
+    deg = (out >= 0).sum(1)
+    present = torch.empty(src.numel(), dtype=torch.bool, device=dev)
+    for a0 in range(0, src.numel(), step):
+        a1 = min(src.numel(), a0 + step)
+        present[a0:a1] = (out[dpos[a0:a1]] == src[a0:a1, None]).any(1)
+    src, dpos = src[~present], dpos[~present]
+    start = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    start[1:] = torch.cumsum(torch.bincount(dpos, minlength=n), 0)
+    rank = torch.arange(dpos.numel(), device=dev) - start[dpos]
+    slot = deg[dpos] + rank
+    ok = slot < R
+    out[dpos[ok], slot[ok]] = src[ok]
+    return out
+
+
 def sample_members(offsets: np.ndarray, nbrs: np.ndarray, ratio: float, seed: int) -> np.ndarray:
     """Uniform node-wise seed sampling + 1-hop expansion until the target ratio
     (seed batch = 1% of N per round); the last
@@ -354,13 +442,13 @@ def sample_members(offsets: np.ndarray, nbrs: np.ndarray, ratio: float, seed: in
     return flags
 
 
-def reconnect(X: torch.Tensor, flags: np.ndarray, R: int, labels=None, metric="l2"):
+def reconnect(X: torch.Tensor, flags: np.ndarray, R: int, labels=None, metric="l2", plain_knn: bool = False):
     """Rebuild edges among members with the same construction.
     Returns the subgraph CSR over the full id space (non-members: empty rows)."""
     N = X.shape[0]
     mem = np.flatnonzero(flags)
     ids = torch.from_numpy(mem).to(X.device)
-    rows = knn_graph(X, R, ids=ids, labels=labels, metric=metric).cpu().numpy()
+    rows = (knn_graph(X, R, ids=ids, labels=labels) if plain_knn else build_graph(X, R, ids=ids, labels=labels)).cpu().numpy()
     return csr_from_rows(rows, N, ids=mem)
 
 
@@ -514,11 +602,11 @@ def build_instance(cfg: Config, device="cpu", with_full_graph: bool = True, gt: 
     if cfg.N > 50_000:               # larger: cluster-local kNN + neighbour-of-neighbour refinement
         use_gen = __import__("os").environ.get("PA_KNN_LABELS", "geo") == "gen" and labels is not None
         lab = labels if use_gen else partition_labels(X, max(1, cfg.N // 1000), cfg.seeds["graph"])
-    full_rows = knn_graph(X, cfg.R, labels=lab, metric="l2")
+    full_rows = build_graph(X, cfg.R, labels=lab) if cfg.shape == "mixture" else knn_graph(X, cfg.R, labels=lab)
     full_off, full_nbrs = csr_from_rows(full_rows.cpu().numpy(), cfg.N)
     del full_rows
     flags = sample_members(full_off, full_nbrs, cfg.ratio, cfg.seeds["sample"])
-    sub_off, sub_nbrs = reconnect(X, flags, cfg.R, labels=lab)
+    sub_off, sub_nbrs = reconnect(X, flags, cfg.R, labels=lab, plain_knn=cfg.shape != "mixture")
     V = fit_svd(X, cfg.seeds["base"])
     Xh = rotate(X, V)
     del X

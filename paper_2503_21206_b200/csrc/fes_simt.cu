@@ -18,8 +18,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_fes_simt(DevIndex ix, SearchArg
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int dps = ix.rdim_pad, E = a.E;
-    // per-warp smem: q'[dps] | C[E]
-    const size_t per_warp = (size_t)dps * 4 + (size_t)E * 8;
+    // per-warp smem: q'[dps] | C[E]   (16-B aligned slices)
+    const size_t per_warp = ((size_t)dps * 4 + (size_t)E * 8 + 15) & ~(size_t)15;
     unsigned char* base = smem_raw + per_warp * w;
     float* qs = reinterpret_cast<float*>(base);
     uint64_t* C = reinterpret_cast<uint64_t*>(base + (size_t)dps * 4);
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_fes_simt(DevIndex ix, SearchArg
 
 int launch_fes(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
     if (a.m == 0) return 0;
-    const size_t per_warp = (size_t)ix.rdim_pad * 4 + (size_t)a.E * 8;
+    const size_t per_warp = ((size_t)ix.rdim_pad * 4 + (size_t)a.E * 8 + 15) & ~(size_t)15;
     const size_t smem = per_warp * kWarps;
     int64_t blocks = (a.m + kWarps - 1) / kWarps;
     if (blocks > 148 * 16) blocks = 148 * 16;
