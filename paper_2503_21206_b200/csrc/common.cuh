@@ -85,10 +85,12 @@ __device__ __forceinline__ int warp_merge(const uint64_t* A, int csz, uint64_t x
 
 // In-place rank merge of the passing lanes' keys (ballot `pb` ≠ 0) into the
 // sorted smem list C[0..csz) with capacity cap ≤ 32·SMAX; returns the new size
-// and (minr) the smallest position a new key landed at.  For every passing key x
-// the warp counts with ef/32 ballots rank_C(x) = #{C < x} and, per C entry, the
-// number of passing keys below it (its right shift); keys are unique so the
-// final positions rank_C(x) + #{passing < x} and i + shift(i) are a permutation.
+// and (minr) the smallest position a new key landed at.  Every passing key is
+// broadcast once; each lane counts how many of them precede each C entry it
+// owns (the entry's right shift) and its own key's rank among them; the key's
+// rank in C is a per-lane binary search.  Keys are unique, so the final
+// positions rank_C(x) + #{passing < x} and i + shift(i) form a permutation and
+// everything moves in place (the old C sits in registers across one __syncwarp).
 template <int SMAX>
 __device__ __forceinline__ int rank_merge(uint64_t* C, int csz, int cap, uint64_t key, bool pass, unsigned pb,
                                           int lane, int& minr) {
@@ -101,24 +103,18 @@ __device__ __forceinline__ int rank_merge(uint64_t* C, int csz, int cap, uint64_
         sh[t] = 0;
     }
     const int np = __popc(pb);
-    int rc = 0, rn = 0;
-    minr = cap;
+    int rn = 0;
     while (pb) {
         const int src = __ffs(pb) - 1;
         pb &= pb - 1;
         const uint64_t x = ((uint64_t)__shfl_sync(kFull, (uint32_t)(key >> 32), src) << 32) |
                            __shfl_sync(kFull, (uint32_t)key, src);
-        int r = 0;
 #pragma unroll
-        for (int t = 0; t < SMAX; ++t) {
-            const bool lt = c[t] < x;
-            sh[t] += lt ? 0 : 1;
-            r += __popc(__ballot_sync(kFull, lt));
-        }
-        if (lane == src) rc = r;
-        minr = min(minr, r);
+        for (int t = 0; t < SMAX; ++t) sh[t] += (x < c[t]) ? 1 : 0;
         rn += (x < key) ? 1 : 0;
     }
+    const int rc = pass ? lower_bound_smem(C, csz, key) : cap;
+    minr = (int)__reduce_min_sync(kFull, (unsigned)rc);
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < SMAX; ++t) {

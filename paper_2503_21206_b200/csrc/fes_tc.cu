@@ -1,0 +1,266 @@
+// a3 + a4 — FES bucketing and within-cell scoring on the tensor cores.
+//
+// Alg 2 assigns one GPU block per cluster and skips the queries
+// routed elsewhere ("allocation-free").  Here:
+//   k_bucket  : stable counting sort of the queries by routed cell → perm,
+//               per-cell query offsets and per-cell 128-query tile offsets (a3).
+//   k_fes_tc  : one CTA per (cell, 128 routed queries) tile — a grouped GEMM
+//               S = Q'_tile · EV_cellᵀ on tcgen05 (kind::tf32, 3xTF32, M = 128,
+//               N = 128 pool entries per pass, accumulator in TMEM), fused with
+//               the selection epilogue: score = ‖e‖² − 2 q'·e (L2) or −q'·e (IP),
+//               per query the E smallest (score, id) keys (Q10: GEMM form is used
+//               for SELECTION only; stage ① recomputes direct-form δ).
+// Every GEMM tile is dense (cell-centric tiling, Table 3 density mn/(r(m+n)),
+// P:L417).
+#include <cstdint>
+
+#include "common.cuh"
+#include "internal.h"
+#include "umma.cuh"
+
+namespace pa {
+
+namespace {
+
+constexpr int kM = 128;
+constexpr int kN = 128;
+constexpr int kThreads = 128;
+constexpr int kMaxR = 64;
+
+// ---------------------------------------------------------------- bucketing
+__global__ void __launch_bounds__(1024, 1) k_bucket(const int32_t* __restrict__ cell, int64_t m, int r,
+                                                    int32_t* __restrict__ perm, int32_t* __restrict__ qoff,
+                                                    int32_t* __restrict__ toff) {
+    __shared__ int cnt[kMaxR], base[kMaxR];
+    __shared__ int wc[32][kMaxR];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int c = tid; c < r; c += blockDim.x) cnt[c] = 0;
+    __syncthreads();
+    for (int64_t i = tid; i < m; i += blockDim.x) atomicAdd(&cnt[cell[i]], 1);
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0, trun = 0;
+        for (int c = 0; c < r; ++c) {
+            base[c] = run;
+            qoff[c] = run;
+            toff[c] = trun;
+            run += cnt[c];
+            trun += (cnt[c] + kM - 1) / kM;
+        }
+        qoff[r] = run;
+        toff[r] = trun;
+    }
+    __syncthreads();
+    for (int64_t t0 = 0; t0 < m; t0 += 1024) {
+        for (int c = lane; c < r; c += 32) wc[w][c] = 0;
+        __syncwarp();
+        const int64_t i = t0 + tid;
+        const bool ok = i < m;
+        const int c = ok ? cell[i] : -1;
+        const unsigned act = __ballot_sync(0xffffffffu, ok);
+        unsigned peers = 0;
+        int rk = 0;
+        if (ok) {
+            peers = __match_any_sync(act, c);
+            rk = __popc(peers & ((1u << lane) - 1u));
+            if (rk == 0) wc[w][c] = __popc(peers);
+        }
+        __syncthreads();
+        for (int cc = tid; cc < r; cc += blockDim.x) {
+            int run = base[cc];
+            for (int ww = 0; ww < 32; ++ww) {
+                const int x = wc[ww][cc];
+                wc[ww][cc] = run;
+                run += x;
+            }
+            base[cc] = run;
+        }
+        __syncthreads();
+        if (ok) perm[wc[w][c] + rk] = (int32_t)i;
+        __syncthreads();
+    }
+}
+
+struct FesParams {
+    const float* qp;
+    int dps, kchunks;
+    const int32_t* perm;
+    const int32_t* qoff;
+    const int32_t* toff;
+    int r;
+    const float* pool_vec;
+    const float* pool_norm;
+    const int32_t* pool_ids;
+    const int32_t* cell_off;
+    int E, metric;
+    int32_t* entries;
+};
+
+template <int METRIC>
+__global__ void __launch_bounds__(kThreads, 1) k_fes_tc(FesParams p) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int t = blockIdx.x;
+    if (t >= p.toff[p.r]) return;
+    int c = 0;
+    while (c + 1 < p.r && p.toff[c + 1] <= t) ++c;
+    const int qbase = p.qoff[c] + (t - p.toff[c]) * kM;
+    const int nrows = min(kM, p.qoff[c + 1] - qbase);
+    const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
+    const int E = p.E, kch = p.kchunks;
+
+    // smem carve-up (1024-B aligned operand tiles)
+    unsigned char* a_hi = smem;                               // kch × 16 KB
+    unsigned char* a_lo = a_hi + kch * 16384;
+    unsigned char* b_hi = a_lo + kch * 16384;                 // 16 KB
+    unsigned char* b_lo = b_hi + 16384;
+    uint64_t* L = reinterpret_cast<uint64_t*>(b_lo + 16384);  // [128][E]
+    float* T = reinterpret_cast<float*>(L + (size_t)kM * E);  // [4][32][33]
+    int* lsz = reinterpret_cast<int*>(T + 4 * 32 * 33);
+    int* rowq = lsz + kM;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(rowq + kM);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+    if (warp == 0) tmem_alloc(tslot, kN);
+    if (tid == 0) mbar_init(bar, 1);
+    // ---- A: this thread's routed query row, hi/lo split, K-major SW128
+    {
+        const int q = tid < nrows ? p.perm[qbase + tid] : -1;
+        rowq[tid] = q;
+        lsz[tid] = 0;
+        for (int kc = 0; kc < kch; ++kc) {
+#pragma unroll 8
+            for (int k = 0; k < 32; ++k) {
+                const int col = kc * 32 + k;
+                const float a = (q >= 0 && col < p.dps) ? __ldg(p.qp + (int64_t)q * p.dps + col) : 0.f;
+                float hi, lo;
+                split_tf32(a, hi, lo);
+                const uint32_t off = (uint32_t)kc * 16384 + sw128_off(tid, k);
+                *reinterpret_cast<float*>(a_hi + off) = hi;
+                *reinterpret_cast<float*>(a_lo + off) = lo;
+            }
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t idesc = make_idesc_tf32(kM, kN);
+    uint32_t phase = 0;
+    float* Tw = T + warp * 32 * 33;
+
+    for (int n0 = 0; n0 < nc; n0 += kN) {
+        for (int kc = 0; kc < kch; ++kc) {
+            // B: 128 pool rows of this cell, K-chunk kc (coalesced along K)
+            for (int idx = tid; idx < kN * 32; idx += kThreads) {
+                const int n = idx >> 5, k = idx & 31;
+                const int col = kc * 32 + k;
+                const float b = (n0 + n < nc && col < p.dps) ? __ldg(p.pool_vec + (int64_t)(pb + n0 + n) * p.dps + col) : 0.f;
+                float hi, lo;
+                split_tf32(b, hi, lo);
+                const uint32_t off = sw128_off(n, k);
+                *reinterpret_cast<float*>(b_hi + off) = hi;
+                *reinterpret_cast<float*>(b_lo + off) = lo;
+            }
+            fence_proxy_async();
+            __syncthreads();
+            if (tid == 0) {
+                tmem_fence_after();
+                const uint32_t sah = smem_u32(a_hi) + kc * 16384, sal = smem_u32(a_lo) + kc * 16384;
+                const uint32_t sbh = smem_u32(b_hi), sbl = smem_u32(b_lo);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t ko = kk * 32;
+                    const uint32_t acc0 = (kc > 0 || kk > 0) ? 1u : 0u;
+                    mma_tf32(tmem, make_desc_sw128(sah + ko), make_desc_sw128(sbh + ko), idesc, acc0);
+                    mma_tf32(tmem, make_desc_sw128(sah + ko), make_desc_sw128(sbl + ko), idesc, 1u);
+                    mma_tf32(tmem, make_desc_sw128(sal + ko), make_desc_sw128(sbh + ko), idesc, 1u);
+                }
+                mma_commit(bar);
+            }
+            __syncwarp();
+            mbar_wait(bar, phase);
+            phase ^= 1;
+        }
+        tmem_fence_after();
+        // ---- selection epilogue: warp w owns rows 32w..32w+31 (TMEM lanes)
+        for (int c0 = 0; c0 < kN; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            const int jb = n0 + c0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int jj = jb + j;
+                float s = 0.f;
+                if (jj < nc) s = METRIC == 0 ? fmaf(-2.f, v[j], __ldg(p.pool_norm + pb + jj)) : -v[j];
+                Tw[lane * 33 + j] = s;
+            }
+            __syncwarp();
+            const bool colok = jb + lane < nc;
+            const int32_t pid = colok ? __ldg(p.pool_ids + pb + jb + lane) : 0;
+            for (int rr = 0; rr < 32; ++rr) {
+                const int row = warp * 32 + rr;
+                if (rowq[row] < 0) continue;
+                uint64_t* Lr = L + (size_t)row * E;
+                const int sz = lsz[row];
+                const uint64_t key = colok ? make_key(Tw[rr * 33 + lane], pid) : kKeyInf;
+                const uint64_t thresh = sz == E ? Lr[E - 1] : kKeyInf;
+                const bool pass = key < thresh;
+                const unsigned pbal = __ballot_sync(kFull, pass);
+                if (pbal == 0) continue;
+                int minr;
+                const int ns = rank_merge<2>(Lr, sz, E, key, pass, pbal, lane, minr);
+                if (lane == 0) lsz[row] = ns;
+                __syncwarp();
+            }
+            __syncwarp();
+        }
+        tmem_fence_before();
+        __syncthreads();
+    }
+    // ---- entries out
+    for (int rr = 0; rr < 32; ++rr) {
+        const int row = warp * 32 + rr;
+        const int q = rowq[row];
+        if (q < 0) continue;
+        const uint64_t* Lr = L + (size_t)row * E;
+        const int sz = lsz[row];
+        for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < sz ? key_id(Lr[j]) : -1;
+    }
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tmem_fence_after();
+        tmem_dealloc(tmem, kN);
+    }
+}
+
+size_t fes_tc_smem(int kch, int E) {
+    return (size_t)kch * 2 * 16384 + 2 * 16384 + (size_t)kM * E * 8 + 4 * 32 * 33 * 4 + 2 * kM * 4 + 16;
+}
+
+}  // namespace
+
+bool fes_tc_supported(const DevIndex& ix, int E) {
+    const int kch = (ix.rdim_pad + 31) / 32;
+    return ix.pool_norm != nullptr && ix.fes_r <= kMaxR && E <= 64 && fes_tc_smem(kch, E) <= 227 * 1024;
+}
+
+int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
+    if (a.m == 0) return 0;
+    k_bucket<<<1, 1024, 0, s>>>(a.cell, a.m, ix.fes_r, a.perm, a.qoff, a.toff);
+    FesParams p;
+    p.qp = a.qp; p.dps = ix.rdim_pad; p.kchunks = (ix.rdim_pad + 31) / 32;
+    p.perm = a.perm; p.qoff = a.qoff; p.toff = a.toff; p.r = ix.fes_r;
+    p.pool_vec = ix.pool_vec; p.pool_norm = ix.pool_norm; p.pool_ids = ix.pool_ids; p.cell_off = ix.cell_off;
+    p.E = a.E; p.metric = ix.metric; p.entries = a.entries;
+    const size_t smem = fes_tc_smem(p.kchunks, a.E);
+    const unsigned grid = (unsigned)((a.m + kM - 1) / kM + ix.fes_r);
+    void* fn = ix.metric == 0 ? (void*)k_fes_tc<0> : (void*)k_fes_tc<1>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void* args[] = {&p};
+    cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
+    return 2;
+}
+
+}  // namespace pa

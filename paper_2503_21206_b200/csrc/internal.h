@@ -22,6 +22,7 @@ struct DevIndex {
     float* pool_vec = nullptr;                 // [pool_n][rdim_pad] contiguous by cell
     float* proj_bt = nullptr;                  // [roundup16(r + dim)][dim] B_T of the tcgen05 projection
     float* cent_norm = nullptr;                // [r] ‖centroid‖²
+    float* pool_norm = nullptr;                // [pool_n] ‖e‖² (GEMM-form FES scores)
 };
 
 struct SearchArgs {
@@ -34,6 +35,9 @@ struct SearchArgs {
     float* qres = nullptr;         // [m][dim − rdim] (optional) residual projection for host stages
     int32_t* cell = nullptr;       // [m]
     bool cell_ready = false;       // routing already computed (by the tcgen05 projection epilogue)
+    int32_t* perm = nullptr;       // [m]   queries bucketed by cell (a3)
+    int32_t* qoff = nullptr;       // [r+1] per-cell query offsets
+    int32_t* toff = nullptr;       // [r+1] per-cell 128-query tile offsets
     int32_t* entries = nullptr;    // [m][E]
     int32_t* cand_ids = nullptr;   // [m][ef] (optional)
     float* cand_d = nullptr;       // [m][ef] (optional)
@@ -58,6 +62,8 @@ int launch_project(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
 int launch_project_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
 bool project_tc_supported(const DevIndex& ix, bool with_qres);
 int launch_fes(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
+int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
+bool fes_tc_supported(const DevIndex& ix, int E);
 int launch_traverse(const DevIndex& ix, const SearchArgs& a, int grid_warps, cudaStream_t s);
 int traverse_max_warps(const DevIndex& ix, const SearchArgs& a);   // resident warps for the launch config
 

@@ -131,7 +131,7 @@ struct pa_index {
     int32_t ws_E = 0, ws_ef = 0, ws_k = 0;
     float *q = nullptr, *qp = nullptr, *qres = nullptr, *cand_d = nullptr, *out_d = nullptr;
     int32_t *cell = nullptr, *entries = nullptr, *cand_ids = nullptr, *out_ids = nullptr, *counters = nullptr,
-            *work = nullptr;
+            *work = nullptr, *perm = nullptr, *qoff = nullptr, *toff = nullptr;
     uint64_t* spill = nullptr;
     int64_t spill_warps = 0;
     int32_t spill_log2 = 16;
@@ -153,9 +153,10 @@ bool live(const pa_index* ix) {
 void free_ws(pa_index* ix) {
     cudaFree(ix->q); cudaFree(ix->qp); cudaFree(ix->qres); cudaFree(ix->cand_d); cudaFree(ix->out_d);
     cudaFree(ix->cell); cudaFree(ix->entries); cudaFree(ix->cand_ids); cudaFree(ix->out_ids);
-    cudaFree(ix->counters); cudaFree(ix->work);
+    cudaFree(ix->counters); cudaFree(ix->work); cudaFree(ix->perm); cudaFree(ix->qoff); cudaFree(ix->toff);
     ix->q = ix->qp = ix->qres = ix->cand_d = ix->out_d = nullptr;
     ix->cell = ix->entries = ix->cand_ids = ix->out_ids = ix->counters = ix->work = nullptr;
+    ix->perm = ix->qoff = ix->toff = nullptr;
     ix->ws_m = 0;
 }
 
@@ -176,6 +177,9 @@ pa_status ensure_ws(pa_index* ix, int64_t m, int32_t E, int32_t ef, int32_t k) {
     CU(dalloc(&ix->out_d, (size_t)m * k));
     CU(dalloc(&ix->counters, (size_t)m * 4));
     CU(dalloc(&ix->work, 4));
+    CU(dalloc(&ix->perm, (size_t)m));
+    CU(dalloc(&ix->qoff, (size_t)d.fes_r + 1));
+    CU(dalloc(&ix->toff, (size_t)d.fes_r + 1));
     ix->ws_m = m; ix->ws_E = E; ix->ws_ef = ef; ix->ws_k = k;
     return PA_OK;
 }
@@ -239,6 +243,7 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     a.counters = (dbg && dbg->counters) ? dbg->counters : ix->counters;
     a.out_ids = d_out_ids; a.out_d = d_out_d;
     a.work = ix->work;
+    a.perm = ix->perm; a.qoff = ix->qoff; a.toff = ix->toff;
     if (dbg && dbg->trace_cap > 0 && dbg->trace_expand && dbg->trace_visit && dbg->trace_nexp && dbg->trace_nvis) {
         a.trace_cap = dbg->trace_cap; a.trace_expand = dbg->trace_expand; a.trace_visit = dbg->trace_visit;
         a.trace_nexp = dbg->trace_nexp; a.trace_nvis = dbg->trace_nvis;
@@ -258,7 +263,8 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
 
     int launches = 0;
     CU(cudaEventRecord(ix->ev[0], s));
-    static const bool force_simt = [] { const char* e = std::getenv("PA_PROJECT"); return e && !std::strcmp(e, "simt"); }();
+    const char* pe = std::getenv("PA_PROJECT");           // A/B and test hooks: "simt" selects the SIMT kernels
+    const bool force_simt = pe && !std::strcmp(pe, "simt");
     if (!force_simt && pa::project_tc_supported(ix->dev, a.qres != nullptr)) {
         launches += pa::launch_project_tc(ix->dev, a, s);
         a.cell_ready = true;
@@ -267,7 +273,12 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     }
     CU(cudaGetLastError());
     CU(cudaEventRecord(ix->ev[1], s));
-    launches += pa::launch_fes(ix->dev, a, s);
+    const char* fe = std::getenv("PA_FES");
+    const bool force_fes_simt = fe && !std::strcmp(fe, "simt");
+    if (a.cell_ready && !force_fes_simt && !(a.flags & PA_NO_FES) && pa::fes_tc_supported(ix->dev, a.E))
+        launches += pa::launch_fes_tc(ix->dev, a, s);
+    else
+        launches += pa::launch_fes(ix->dev, a, s);
     CU(cudaGetLastError());
     CU(cudaEventRecord(ix->ev[2], s));
     launches += pa::launch_traverse(ix->dev, a, (int)gridw, s);
@@ -464,6 +475,15 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
             std::memcpy(&pv[(size_t)j * dps], p->reduced + (int64_t)p->fes_pool_ids[j] * dp, sizeof(float) * dp);
         CUB(dalloc(&d.pool_vec, pv.size()));
         CUB(cudaMemcpy(d.pool_vec, pv.data(), sizeof(float) * pv.size(), cudaMemcpyHostToDevice));
+        std::vector<float> pn((size_t)pool_n);
+        for (int64_t j = 0; j < pool_n; ++j) {
+            double s2 = 0;
+            const float* e = p->reduced + (int64_t)p->fes_pool_ids[j] * dp;
+            for (int i = 0; i < dp; ++i) s2 += (double)e[i] * e[i];
+            pn[j] = (float)s2;
+        }
+        CUB(dalloc(&d.pool_norm, pn.size()));
+        CUB(cudaMemcpy(d.pool_norm, pn.data(), sizeof(float) * pn.size(), cudaMemcpyHostToDevice));
     }
     // tcgen05 projection operand B_T = [(V_{:d'}·Cᵀ)ᵀ ; Vᵀ] (rows K-major), fp64 → fp32, zero-padded
     {
@@ -648,7 +668,7 @@ void pa_destroy(pa_index* ix) {
     cudaFreeHost(ix->h_counters);
     auto& d = ix->dev;
     cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
-    cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm);
+    cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
     if (ix->stream) cudaStreamDestroy(ix->stream);
     ix->magic = 0;

@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "umma.cuh"
 
 namespace pa {
 
@@ -29,78 +30,6 @@ namespace {
 constexpr int kM = 128;        // UMMA M (queries per CTA)
 constexpr int kKC = 32;        // K floats per smem chunk (128 B, one swizzle atom column)
 constexpr int kThreads = 128;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// Byte offset of element (row, k) of a [rows][32] fp32 K-major SWIZZLE_128B tile.
-__device__ __forceinline__ uint32_t sw128_off(int row, int k) {
-    const int chunk = k >> 2;                       // 16-B chunk within the 128-B row
-    return (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4) + ((k & 3) << 2));
-}
-
-// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B, LBO = 16 B (unused), version 1.
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr & 0x3FFFF) >> 4);        // start address [0,14)
-    d |= (uint64_t)1 << 16;                         // LBO (16 B)       [16,30)
-    d |= (uint64_t)(1024 >> 4) << 32;               // SBO (1024 B)     [32,46)
-    d |= (uint64_t)1 << 46;                         // version = 1      [46,48)
-    d |= (uint64_t)2 << 61;                         // SWIZZLE_128B     [61,64)
-    return d;
-}
-
-// Instruction descriptor, kind::tf32: D = F32, A = B = TF32, both K-major, M = 128, N.
-__device__ __forceinline__ uint32_t make_idesc(int N) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
-        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                 :: "r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}\n"
-        :: "r"(smem_u32(bar)), "r"(phase) : "memory");
-}
-
-__device__ __forceinline__ void split_tf32(float a, float& hi, float& lo) {
-    hi = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
-    lo = a - hi;
-}
-
-// TMEM → registers: 16 consecutive fp32 columns of this thread's lane.
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 struct ProjParams {
     const float* q;        // [m][D]
@@ -118,7 +47,7 @@ struct ProjParams {
 // Dynamic smem: A_hi | A_lo (16 KB each) | B_hi | B_lo (ncols_pad × 128 B each) | mbarrier | tmem slot
 __global__ void __launch_bounds__(kThreads, 1) k_project_tc(ProjParams p) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const int ncols = p.ncols;
     const int bbytes = ncols * 128;
     unsigned char* a_hi = smem;
@@ -131,15 +60,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_project_tc(ProjParams p) {
     // TMEM columns: power of two ≥ 32 covering ncols (≤ 512)
     uint32_t tcols = 32;
     while ((int)tcols < ncols) tcols <<= 1;
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(smem_u32(tslot)), "r"(tcols) : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    if (warp == 0) tmem_alloc(tslot, tcols);
+    if (tid == 0) mbar_init(bar, 1);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -184,14 +106,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_project_tc(ProjParams p) {
             const uint32_t sb_hi = smem_u32(b_hi), sb_lo = smem_u32(b_lo);
             for (int n0 = 0; n0 < ncols; n0 += 256) {
                 const int nn = min(256, ncols - n0);
-                const uint32_t idesc = make_idesc(nn);
+                const uint32_t idesc = make_idesc_tf32(kM, nn);
                 const uint32_t td = tmem + (uint32_t)n0;
 #pragma unroll
                 for (int kk = 0; kk < kKC / 8; ++kk) {
                     const uint32_t koff = (uint32_t)kk * 32;       // 8 tf32 = 32 B along K
                     const uint32_t boff = (uint32_t)n0 * 128;
-                    const uint64_t ah = make_desc(sa_hi + koff), al = make_desc(sa_lo + koff);
-                    const uint64_t bh = make_desc(sb_hi + boff + koff), bl = make_desc(sb_lo + boff + koff);
+                    const uint64_t ah = make_desc_sw128(sa_hi + koff), al = make_desc_sw128(sa_lo + koff);
+                    const uint64_t bh = make_desc_sw128(sb_hi + boff + koff), bl = make_desc_sw128(sb_lo + boff + koff);
                     const uint32_t acc0 = (ch > 0 || kk > 0) ? 1u : 0u;
                     mma_tf32(td, ah, bh, idesc, acc0);
                     mma_tf32(td, ah, bl, idesc, 1u);
@@ -237,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_project_tc(ProjParams p) {
     __syncthreads();
     if (warp == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tcols) : "memory");
+        tmem_dealloc(tmem, tcols);
     }
 }
 

@@ -77,8 +77,22 @@ __device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& 
     return false;   // unreachable while count2 ≤ gmask/2 (guarded by the caller)
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+// Bulk prefetch of one reduced-vector row into L2 (sm_90+ cp.async.bulk.prefetch).
+__device__ __forceinline__ void prefetch_row_l2(const void* p, int bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+
+// Lookup-only probe of the level-1 hash (speculation; false negatives only cost a prefetch).
+__device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
+    const uint32_t S = 1u << vs.log2S;
+    uint32_t h = hash1(v) >> (32 - vs.log2S);
+    for (uint32_t p = 0; p < 8; ++p) {
+        const int32_t cur = vs.H[h];
+        if (cur == v) return true;
+        if (cur == -1) return false;
+        h = (h + 1) & (S - 1);
+    }
+    return false;
 }
 
 template <int METRIC, int ELLW, int SMAX, bool TRACE>
@@ -117,11 +131,11 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
 
         int csz = 0, hint = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
 
-        // One batch of ≤32 candidate ids (one per lane, −1 = none): visited
-        // test-and-insert, δ' for new ids, rank-merge of the keys that beat C's worst.
-        auto batch = [&](int32_t v) {
+        // Visited test-and-insert for one batch of ≤32 candidate ids (one per
+        // lane, −1 = none); returns whether this lane's id is new (Alg 1 l.6-7).
+        auto visit_batch = [&](int32_t v) -> bool {
             const bool open1 = vs.count1 + 32 <= cap1;
-            if (!open1 && vs.count2 + 32 > cap2) { status = 1; return; }
+            if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
             bool l2 = false;
             const bool isnew = v >= 0 && visit(vs, v, open1, l2);
             const unsigned bal = __ballot_sync(kFull, isnew);
@@ -134,12 +148,16 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
                 if (pos < a.trace_cap) a.trace_visit[q * a.trace_cap + pos] = v;
             }
             n_dist += nnew;
-            if (nnew == 0) return;
+            return isnew;
+        };
+        // δ' for the new ids (l.8) and rank-merge of the keys that beat C's worst (l.9, l.11).
+        auto merge_batch = [&](int32_t v, bool isnew) {
+            if (__ballot_sync(kFull, isnew) == 0) return;
             uint64_t key = kKeyInf;
             if (isnew) key = make_key(row_dist<METRIC>(qs, ix.reduced + (int64_t)v * dps, dps), v);
             const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
             const bool pass = key < thresh;                   // unique keys: strict
-            unsigned pb = __ballot_sync(kFull, pass);
+            const unsigned pb = __ballot_sync(kFull, pass);
             if (pb == 0) return;
             int minr;
             csz = rank_merge<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
@@ -148,10 +166,21 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
 
         // ---- a5: C := entries (Alg 1 l.3), visited := entries (Q15)
         for (int j0 = 0; j0 < a.E && status == 0; j0 += 32) {
-            int j = j0 + lane;
-            batch(j < a.E ? a.entries[q * a.E + j] : -1);
+            const int j = j0 + lane;
+            const int32_t v = j < a.E ? a.entries[q * a.E + j] : -1;
+            const bool isnew = visit_batch(v);
+            if (status == 0) merge_batch(v, isnew);
         }
-        // ---- a6: Alg 1 l.4-12
+        // ---- a6: Alg 1 l.4-12.  Speculation: the runner-up unchecked node u2 is
+        // the likely next expansion; its ELL row is loaded into registers (sv)
+        // alongside u's, and the reduced rows of its not-yet-visited neighbours
+        // are prefetched into L2 while u's distances are computed.  A correct
+        // guess makes the next iteration's two dependent loads L2 hits; a wrong
+        // guess only costs bandwidth.  The algorithm's decisions are unchanged.
+        int32_t spec_u = -1;
+        int32_t sv[ELLW / 32];
+#pragma unroll
+        for (int c = 0; c < ELLW / 32; ++c) sv[c] = -1;
         if (!(a.flags & 4u)) {
             for (int it = 0; status == 0; ++it) {
                 int p = -1, p2 = -1;
@@ -169,11 +198,22 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
                 if (p < 0) break;                                   // l.12: no unchecked node
                 const uint64_t ku = C[p];
                 const int32_t u = key_id(ku);
-                const int32_t* row = ix.ell + (int64_t)u * ELLW;
                 int32_t vv[ELLW / 32];
+                if (u == spec_u) {
 #pragma unroll
-                for (int c = 0; c < ELLW / 32; ++c) vv[c] = __ldg(row + c * 32 + lane);
-                if (p2 >= 0 && lane == 0) prefetch_l2(ix.ell + (int64_t)key_id(C[p2]) * ELLW);
+                    for (int c = 0; c < ELLW / 32; ++c) vv[c] = sv[c];
+                } else {
+                    const int32_t* row = ix.ell + (int64_t)u * ELLW;
+#pragma unroll
+                    for (int c = 0; c < ELLW / 32; ++c) vv[c] = __ldg(row + c * 32 + lane);
+                }
+                const int32_t u2 = p2 >= 0 ? key_id(C[p2]) : -1;
+                if (u2 >= 0) {
+                    const int32_t* row2 = ix.ell + (int64_t)u2 * ELLW;
+#pragma unroll
+                    for (int c = 0; c < ELLW / 32; ++c) sv[c] = __ldg(row2 + c * 32 + lane);
+                }
+                spec_u = u2;
                 __syncwarp();
                 if (lane == 0) C[p] = ku | 1ull;                    // mark checked
                 hint = p + 1;
@@ -182,7 +222,17 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
                 __syncwarp();
 #pragma unroll
                 for (int c = 0; c < ELLW / 32; ++c) {
-                    if (status == 0) batch(vv[c]);
+                    if (status != 0) break;
+                    const bool isnew = visit_batch(vv[c]);
+                    if (c == 0 && u2 >= 0) {
+#pragma unroll
+                        for (int c2 = 0; c2 < ELLW / 32; ++c2) {
+                            const int32_t w2 = sv[c2];
+                            if (w2 >= 0 && !visited_l1(vs, w2))
+                                prefetch_row_l2(ix.reduced + (int64_t)w2 * dps, dps * 4);
+                        }
+                    }
+                    if (status == 0) merge_batch(vv[c], isnew);
                 }
                 if (it >= kIterCap) status = 2;
             }

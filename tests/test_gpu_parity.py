@@ -172,3 +172,21 @@ def test_host_path_equals_device_path(s1):
         ix2.search(s1["queries"], k=10, ef=64)
     assert e.value.status == pa.PA_ESTATE
     ix2._h = None
+
+
+@pytest.mark.parametrize("cfg_name", ["S1", "S2"])
+def test_tensor_core_paths_match_simt(cfg_name, request, monkeypatch):
+    """tcgen05 projection+routing and tcgen05 FES select the same cells/entries as
+    the SIMT kernels except at GEMM-form near-ties; q' agrees to ~fp32 rounding."""
+    inst = request.getfixturevalue(cfg_name.lower())
+    cfg = inst["cfg"]
+    ix = pa.Index.from_instance(inst)
+    tc = run_gpu(ix, inst, cfg.k, cfg.ef)
+    monkeypatch.setenv("PA_PROJECT", "simt")
+    monkeypatch.setenv("PA_FES", "simt")
+    si = run_gpu(ix, inst, cfg.k, cfg.ef)
+    ix.close()
+    assert (tc["cell"] == si["cell"]).mean() >= 0.98
+    same = np.array([set(a) == set(b) for a, b in zip(tc["entries"], si["entries"])])
+    assert same.mean() >= 0.95, same.mean()
+    assert orc.recall(tc["ids"], si["ids"], cfg.k) >= 0.97
