@@ -106,8 +106,9 @@ def make_instance(cfg_name, world, rank, m_per_rank, cache=None):
         log(f"[rank {rank}] instance loaded from {path} in {time.time() - t0:.1f}s")
         return cfg, inst
     inst = dg.build_instance(cfg, device=f"cuda:{torch.cuda.current_device()}", gt=False)
+    from paper_2503_21206_b200.dist import shard_bounds
     Q = inst["queries"]
-    lo, hi = rank * m_per_rank, (rank + 1) * m_per_rank
+    lo, hi = shard_bounds(Q.shape[0], rank, world)
     inst["queries"] = np.ascontiguousarray(Q[lo:hi])
     # ground truths for this rank's shard (exhaustive scan; recall measurement only)
     dev = f"cuda:{torch.cuda.current_device()}"
@@ -146,10 +147,18 @@ def run_reference(args, rank, world):
     orc.build()
     torch.cuda.set_device(0) if torch.cuda.is_available() else None
     cfg, inst = make_instance(args.config, 1, 0, args.m) if torch.cuda.is_available() else make_cpu_instance(args)
-    ef = args.ef or 64
     cores = os.cpu_count()
     sample = args.ref_sample
     Q = inst["queries"]
+    ef = args.ef
+    if not ef:                       # same operating-point rule as the GPU arm, on a sample
+        probe = min(len(Q), 500)
+        for e in EF_SWEEP:
+            rr = orc.search(inst, queries=Q[:probe], k=cfg.k, ef=e, stages=1)
+            if recall_at(rr["ids"], inst["gt_sub_ids"][:probe], cfg.k) >= TARGET_RECALL:
+                ef = e
+                break
+        ef = ef or EF_SWEEP[-1]
     for _ in range(args.warmup):
         orc.search(inst, queries=Q[:min(sample, 64)], k=cfg.k, ef=ef, stages=1)
     times = []
@@ -234,7 +243,7 @@ def run_ours(args, rank, world, local_rank):
         step(ef)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    trav_ms, launches, bytes_alg = [], 0, 0.0
+    trav_ms, proj_ms, fes_ms, launches, bytes_alg = [], [], [], 0, 0.0
     ell_w = 32 if int(np.diff(inst["sub_offsets"]).max()) <= 32 else 64
     if world > 1:
         dist.barrier()
@@ -247,6 +256,8 @@ def run_ours(args, rank, world, local_rank):
             ev[i][1].record(stream)
             st = ix.stats()                       # syncs the traversal events of this step
             trav_ms.append(st["ms_traverse"])
+            proj_ms.append(st["ms_project"])
+            fes_ms.append(st["ms_fes"])
             launches += st["kernel_launches"]
             bytes_alg = st["sum_n_exp"] * 4 * ell_w + st["sum_n_dist"] * 4 * cfg.dp
         torch.cuda.synchronize()
@@ -305,6 +316,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "kernel": "k_traverse", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
                          "traverse_ms": round(trav, 4), "alg_bytes_per_launch": bytes_alg,
+                         "kernel_ms": {"project": round(sum(proj_ms) / len(proj_ms), 4),
+                                       "fes": round(sum(fes_ms) / len(fes_ms), 4), "traverse": round(trav, 4)},
                          "bytes_model": "sum_q n_exp*4*ELLW + n_dist*4*d'", "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": m * cfg.D * 4,

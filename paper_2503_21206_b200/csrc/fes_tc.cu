@@ -4,12 +4,14 @@
 // routed elsewhere ("allocation-free").  Here:
 //   k_bucket  : stable counting sort of the queries by routed cell → perm,
 //               per-cell query offsets and per-cell 128-query tile offsets (a3).
-//   k_fes_tc  : one CTA per (cell, 128 routed queries) tile — a grouped GEMM
+//   k_fes_scores : one CTA per (cell, 128 routed queries) tile — a grouped GEMM
 //               S = Q'_tile · EV_cellᵀ on tcgen05 (kind::tf32, 3xTF32, M = 128,
-//               N = 128 pool entries per pass, accumulator in TMEM), fused with
-//               the selection epilogue: score = ‖e‖² − 2 q'·e (L2) or −q'·e (IP),
-//               per query the E smallest (score, id) keys (Q10: GEMM form is used
-//               for SELECTION only; stage ① recomputes direct-form δ).
+//               N = 128 pool entries per pass, accumulator in TMEM); epilogue
+//               score = ‖e‖² − 2 q'·e (L2) or −q'·e (IP) → global scratch.
+//   k_fes_select : one warp per query keeps the E smallest (score, id) keys
+//               (Q10: the GEMM form is used for SELECTION only; stage ①
+//               recomputes direct-form δ).  Splitting the selection out keeps
+//               32+ warps per SM on it instead of the 4 epilogue warps of a tile.
 // Every GEMM tile is dense (cell-centric tiling, Table 3 density mn/(r(m+n)),
 // P:L417).
 #include <cstdint>
@@ -28,7 +30,7 @@ constexpr int kThreads = 128;
 constexpr int kMaxR = 64;
 
 // ---------------------------------------------------------------- bucketing
-__global__ void __launch_bounds__(1024, 1) k_bucket(const int32_t* __restrict__ cell, int64_t m, int r,
+__global__ void __launch_bounds__(1024, 1) k_bucket(const int32_t* __restrict__ cell, int64_t m, int r, int mq,
                                                     int32_t* __restrict__ perm, int32_t* __restrict__ qoff,
                                                     int32_t* __restrict__ toff) {
     __shared__ int cnt[kMaxR], base[kMaxR];
@@ -45,7 +47,7 @@ __global__ void __launch_bounds__(1024, 1) k_bucket(const int32_t* __restrict__ 
             qoff[c] = run;
             toff[c] = trun;
             run += cnt[c];
-            trun += (cnt[c] + kM - 1) / kM;
+            trun += (cnt[c] + mq - 1) / mq;
         }
         qoff[r] = run;
         toff[r] = trun;
@@ -92,42 +94,41 @@ struct FesParams {
     const float* pool_norm;
     const int32_t* pool_ids;
     const int32_t* cell_off;
-    int E, metric;
+    int metric;
+    float* scores;               // [m][sstride] GEMM-form scores, row = bucketed position
+    int sstride;                 // ≥ max cell size, multiple of 4
+    int E;
     int32_t* entries;
 };
 
+// Grouped GEMM: one CTA per (cell, 128 bucketed queries) tile; scores of the
+// tile against every pool entry of the cell → global scratch (row = bucketed
+// position).  A = routed q' rows (hi/lo, resident for the tile), B = 128 pool
+// rows per pass; epilogue = tcgen05.ld + ‖e‖² − 2·acc (L2) / −acc (IP).
 template <int METRIC>
-__global__ void __launch_bounds__(kThreads, 1) k_fes_tc(FesParams p) {
+__global__ void __launch_bounds__(kThreads, 1) k_fes_scores(FesParams p) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const int t = blockIdx.x;
     if (t >= p.toff[p.r]) return;
     int c = 0;
     while (c + 1 < p.r && p.toff[c + 1] <= t) ++c;
-    const int qbase = p.qoff[c] + (t - p.toff[c]) * kM;
-    const int nrows = min(kM, p.qoff[c + 1] - qbase);
+    const int pos0 = p.qoff[c] + (t - p.toff[c]) * kM;
+    const int nrows = min(kM, p.qoff[c + 1] - pos0);
     const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
-    const int E = p.E, kch = p.kchunks;
+    const int kch = p.kchunks;
 
-    // smem carve-up (1024-B aligned operand tiles)
     unsigned char* a_hi = smem;                               // kch × 16 KB
     unsigned char* a_lo = a_hi + kch * 16384;
     unsigned char* b_hi = a_lo + kch * 16384;                 // 16 KB
     unsigned char* b_lo = b_hi + 16384;
-    uint64_t* L = reinterpret_cast<uint64_t*>(b_lo + 16384);  // [128][E]
-    float* T = reinterpret_cast<float*>(L + (size_t)kM * E);  // [4][32][33]
-    int* lsz = reinterpret_cast<int*>(T + 4 * 32 * 33);
-    int* rowq = lsz + kM;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(rowq + kM);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(b_lo + 16384);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
     if (warp == 0) tmem_alloc(tslot, kN);
     if (tid == 0) mbar_init(bar, 1);
-    // ---- A: this thread's routed query row, hi/lo split, K-major SW128
     {
-        const int q = tid < nrows ? p.perm[qbase + tid] : -1;
-        rowq[tid] = q;
-        lsz[tid] = 0;
+        const int q = tid < nrows ? p.perm[pos0 + tid] : -1;
         for (int kc = 0; kc < kch; ++kc) {
 #pragma unroll 8
             for (int k = 0; k < 32; ++k) {
@@ -147,11 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fes_tc(FesParams p) {
     const uint32_t tmem = *tslot;
     const uint32_t idesc = make_idesc_tf32(kM, kN);
     uint32_t phase = 0;
-    float* Tw = T + warp * 32 * 33;
+    const int row = tid;                                      // TMEM lane = tile row
+    float* srow = p.scores + (int64_t)(pos0 + row) * p.sstride;
 
     for (int n0 = 0; n0 < nc; n0 += kN) {
         for (int kc = 0; kc < kch; ++kc) {
-            // B: 128 pool rows of this cell, K-chunk kc (coalesced along K)
             for (int idx = tid; idx < kN * 32; idx += kThreads) {
                 const int n = idx >> 5, k = idx & 31;
                 const int col = kc * 32 + k;
@@ -163,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fes_tc(FesParams p) {
                 *reinterpret_cast<float*>(b_lo + off) = lo;
             }
             fence_proxy_async();
+            tmem_fence_before();
             __syncthreads();
             if (tid == 0) {
                 tmem_fence_after();
@@ -183,49 +185,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_fes_tc(FesParams p) {
             phase ^= 1;
         }
         tmem_fence_after();
-        // ---- selection epilogue: warp w owns rows 32w..32w+31 (TMEM lanes)
         for (int c0 = 0; c0 < kN; c0 += 32) {
             float v[32];
             tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
             const int jb = n0 + c0;
+            if (row < nrows && jb < nc) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const int jj = jb + j;
-                float s = 0.f;
-                if (jj < nc) s = METRIC == 0 ? fmaf(-2.f, v[j], __ldg(p.pool_norm + pb + jj)) : -v[j];
-                Tw[lane * 33 + j] = s;
+                for (int j = 0; j < 32; j += 4) {
+                    float4 o;
+                    float* op = &o.x;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int jj = jb + j + u;
+                        const float sc = METRIC == 0 ? fmaf(-2.f, v[j + u], jj < nc ? __ldg(p.pool_norm + pb + jj) : 0.f)
+                                                     : -v[j + u];
+                        op[u] = sc;
+                    }
+                    if (jb + j < nc) *reinterpret_cast<float4*>(srow + jb + j) = o;
+                }
             }
-            __syncwarp();
-            const bool colok = jb + lane < nc;
-            const int32_t pid = colok ? __ldg(p.pool_ids + pb + jb + lane) : 0;
-            for (int rr = 0; rr < 32; ++rr) {
-                const int row = warp * 32 + rr;
-                if (rowq[row] < 0) continue;
-                uint64_t* Lr = L + (size_t)row * E;
-                const int sz = lsz[row];
-                const uint64_t key = colok ? make_key(Tw[rr * 33 + lane], pid) : kKeyInf;
-                const uint64_t thresh = sz == E ? Lr[E - 1] : kKeyInf;
-                const bool pass = key < thresh;
-                const unsigned pbal = __ballot_sync(kFull, pass);
-                if (pbal == 0) continue;
-                int minr;
-                const int ns = rank_merge<2>(Lr, sz, E, key, pass, pbal, lane, minr);
-                if (lane == 0) lsz[row] = ns;
-                __syncwarp();
-            }
-            __syncwarp();
         }
-        tmem_fence_before();
-        __syncthreads();
-    }
-    // ---- entries out
-    for (int rr = 0; rr < 32; ++rr) {
-        const int row = warp * 32 + rr;
-        const int q = rowq[row];
-        if (q < 0) continue;
-        const uint64_t* Lr = L + (size_t)row * E;
-        const int sz = lsz[row];
-        for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < sz ? key_id(Lr[j]) : -1;
     }
     tmem_fence_before();
     __syncthreads();
@@ -235,32 +214,73 @@ __global__ void __launch_bounds__(kThreads, 1) k_fes_tc(FesParams p) {
     }
 }
 
-size_t fes_tc_smem(int kch, int E) {
-    return (size_t)kch * 2 * 16384 + 2 * 16384 + (size_t)kM * E * 8 + 4 * 32 * 33 * 4 + 2 * kM * 4 + 16;
+// Selection: one warp per bucketed query — E smallest (score, pool id) keys over
+// its cell's scores, kept sorted by the same threshold filter + rank merge as
+// the traversal (common.cuh).
+template <int SMAX>
+__global__ void __launch_bounds__(128) k_fes_select(FesParams p, int64_t m) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int E = p.E;
+    uint64_t* C = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)w * E;
+    const int64_t nwarps = (int64_t)gridDim.x * 4;
+    for (int64_t pos = (int64_t)blockIdx.x * 4 + w; pos < m; pos += nwarps) {
+        int c = 0;
+        while (c + 1 < p.r && p.qoff[c + 1] <= pos) ++c;
+        const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
+        const float* srow = p.scores + pos * p.sstride;
+        int csz = 0;
+        for (int j0 = 0; j0 < nc; j0 += 32) {
+            const int j = j0 + lane;
+            const uint64_t key = j < nc ? make_key(srow[j], __ldg(p.pool_ids + pb + j)) : kKeyInf;
+            const uint64_t thresh = csz == E ? C[E - 1] : kKeyInf;
+            const bool pass = key < thresh;
+            const unsigned pbal = __ballot_sync(kFull, pass);
+            if (pbal == 0) continue;
+            int minr;
+            csz = rank_merge<SMAX>(C, csz, E, key, pass, pbal, lane, minr);
+        }
+        const int32_t q = p.perm[pos];
+        for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < csz ? key_id(C[j]) : -1;
+        __syncwarp();
+    }
 }
+
+size_t fes_scores_smem(int kch) { return (size_t)kch * 2 * 16384 + 2 * 16384 + 16; }
 
 }  // namespace
 
 bool fes_tc_supported(const DevIndex& ix, int E) {
     const int kch = (ix.rdim_pad + 31) / 32;
-    return ix.pool_norm != nullptr && ix.fes_r <= kMaxR && E <= 64 && fes_tc_smem(kch, E) <= 227 * 1024;
+    return ix.pool_norm != nullptr && ix.fes_r <= kMaxR && E <= 256 && fes_scores_smem(kch) <= 227 * 1024;
+}
+
+size_t fes_tc_scratch_floats(const DevIndex& ix, int64_t m) {
+    return (size_t)m * (size_t)ix.max_cell;
 }
 
 int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
     if (a.m == 0) return 0;
-    k_bucket<<<1, 1024, 0, s>>>(a.cell, a.m, ix.fes_r, a.perm, a.qoff, a.toff);
+    k_bucket<<<1, 1024, 0, s>>>(a.cell, a.m, ix.fes_r, kM, a.perm, a.qoff, a.toff);
     FesParams p;
     p.qp = a.qp; p.dps = ix.rdim_pad; p.kchunks = (ix.rdim_pad + 31) / 32;
     p.perm = a.perm; p.qoff = a.qoff; p.toff = a.toff; p.r = ix.fes_r;
     p.pool_vec = ix.pool_vec; p.pool_norm = ix.pool_norm; p.pool_ids = ix.pool_ids; p.cell_off = ix.cell_off;
-    p.E = a.E; p.metric = ix.metric; p.entries = a.entries;
-    const size_t smem = fes_tc_smem(p.kchunks, a.E);
+    p.metric = ix.metric; p.scores = a.fes_scores; p.sstride = ix.max_cell; p.E = a.E; p.entries = a.entries;
+    const size_t smem = fes_scores_smem(p.kchunks);
     const unsigned grid = (unsigned)((a.m + kM - 1) / kM + ix.fes_r);
-    void* fn = ix.metric == 0 ? (void*)k_fes_tc<0> : (void*)k_fes_tc<1>;
+    void* fn = ix.metric == 0 ? (void*)k_fes_scores<0> : (void*)k_fes_scores<1>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&p};
     cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
-    return 2;
+    void* sel = a.E <= 64 ? (void*)k_fes_select<2> : a.E <= 128 ? (void*)k_fes_select<4> : (void*)k_fes_select<8>;
+    const size_t ssm = (size_t)4 * a.E * 8;
+    cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    int64_t blocks = (a.m + 3) / 4;
+    int64_t m = a.m;
+    void* args2[] = {&p, &m};
+    cudaLaunchKernel(sel, dim3((unsigned)blocks), dim3(128), args2, ssm, s);
+    return 3;
 }
 
 }  // namespace pa

@@ -23,6 +23,7 @@ struct DevIndex {
     float* proj_bt = nullptr;                  // [roundup16(r + dim)][dim] B_T of the tcgen05 projection
     float* cent_norm = nullptr;                // [r] ‖centroid‖²
     float* pool_norm = nullptr;                // [pool_n] ‖e‖² (GEMM-form FES scores)
+    int32_t max_cell = 0;                      // largest FES cell (score scratch row stride, multiple of 4)
 };
 
 struct SearchArgs {
@@ -38,6 +39,7 @@ struct SearchArgs {
     int32_t* perm = nullptr;       // [m]   queries bucketed by cell (a3)
     int32_t* qoff = nullptr;       // [r+1] per-cell query offsets
     int32_t* toff = nullptr;       // [r+1] per-cell 128-query tile offsets
+    float* fes_scores = nullptr;   // [m][max_cell] GEMM-form FES scores (tcgen05 path scratch)
     int32_t* entries = nullptr;    // [m][E]
     int32_t* cand_ids = nullptr;   // [m][ef] (optional)
     float* cand_d = nullptr;       // [m][ef] (optional)
@@ -64,6 +66,7 @@ bool project_tc_supported(const DevIndex& ix, bool with_qres);
 int launch_fes(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
 int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);
 bool fes_tc_supported(const DevIndex& ix, int E);
+size_t fes_tc_scratch_floats(const DevIndex& ix, int64_t m);
 int launch_traverse(const DevIndex& ix, const SearchArgs& a, int grid_warps, cudaStream_t s);
 int traverse_max_warps(const DevIndex& ix, const SearchArgs& a);   // resident warps for the launch config
 

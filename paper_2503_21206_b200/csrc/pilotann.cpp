@@ -132,6 +132,7 @@ struct pa_index {
     float *q = nullptr, *qp = nullptr, *qres = nullptr, *cand_d = nullptr, *out_d = nullptr;
     int32_t *cell = nullptr, *entries = nullptr, *cand_ids = nullptr, *out_ids = nullptr, *counters = nullptr,
             *work = nullptr, *perm = nullptr, *qoff = nullptr, *toff = nullptr;
+    float* fes_scores = nullptr;
     uint64_t* spill = nullptr;
     int64_t spill_warps = 0;
     int32_t spill_log2 = 16;
@@ -154,6 +155,8 @@ void free_ws(pa_index* ix) {
     cudaFree(ix->q); cudaFree(ix->qp); cudaFree(ix->qres); cudaFree(ix->cand_d); cudaFree(ix->out_d);
     cudaFree(ix->cell); cudaFree(ix->entries); cudaFree(ix->cand_ids); cudaFree(ix->out_ids);
     cudaFree(ix->counters); cudaFree(ix->work); cudaFree(ix->perm); cudaFree(ix->qoff); cudaFree(ix->toff);
+    cudaFree(ix->fes_scores);
+    ix->fes_scores = nullptr;
     ix->q = ix->qp = ix->qres = ix->cand_d = ix->out_d = nullptr;
     ix->cell = ix->entries = ix->cand_ids = ix->out_ids = ix->counters = ix->work = nullptr;
     ix->perm = ix->qoff = ix->toff = nullptr;
@@ -180,6 +183,7 @@ pa_status ensure_ws(pa_index* ix, int64_t m, int32_t E, int32_t ef, int32_t k) {
     CU(dalloc(&ix->perm, (size_t)m));
     CU(dalloc(&ix->qoff, (size_t)d.fes_r + 1));
     CU(dalloc(&ix->toff, (size_t)d.fes_r + 1));
+    CU(dalloc(&ix->fes_scores, pa::fes_tc_scratch_floats(d, m)));
     ix->ws_m = m; ix->ws_E = E; ix->ws_ef = ef; ix->ws_k = k;
     return PA_OK;
 }
@@ -243,7 +247,7 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     a.counters = (dbg && dbg->counters) ? dbg->counters : ix->counters;
     a.out_ids = d_out_ids; a.out_d = d_out_d;
     a.work = ix->work;
-    a.perm = ix->perm; a.qoff = ix->qoff; a.toff = ix->toff;
+    a.perm = ix->perm; a.qoff = ix->qoff; a.toff = ix->toff; a.fes_scores = ix->fes_scores;
     if (dbg && dbg->trace_cap > 0 && dbg->trace_expand && dbg->trace_visit && dbg->trace_nexp && dbg->trace_nvis) {
         a.trace_cap = dbg->trace_cap; a.trace_expand = dbg->trace_expand; a.trace_visit = dbg->trace_visit;
         a.trace_nexp = dbg->trace_nexp; a.trace_nvis = dbg->trace_nvis;
@@ -382,6 +386,8 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     for (int c = 0; c < r; ++c)
         if (p->fes_cell_off[c + 1] <= p->fes_cell_off[c]) return fail(PA_EFES, "FES cell %d is empty", c);
     const int64_t pool_n = p->fes_cell_off[r];
+    int64_t max_cell = 0;
+    for (int c = 0; c < r; ++c) max_cell = std::max<int64_t>(max_cell, p->fes_cell_off[c + 1] - p->fes_cell_off[c]);
     if (pool_n >= (1ll << 31)) return fail(PA_EFES, "pool too large");
     {
         std::vector<uint8_t> seen(n, 0);
@@ -412,6 +418,7 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     auto& d = ix->dev;
     d.n = n; d.dim = D; d.rdim = dp; d.rdim_pad = (dp + 3) & ~3; d.metric = p->metric; d.fes_r = r;
     d.pool_n = pool_n;
+    d.max_cell = (int32_t)((max_cell + 3) & ~3);
     d.ell_w = p->max_degree <= 32 ? 32 : 64;
     const int dps = d.rdim_pad;
     auto bail = [&](pa_status s) { pa_destroy(ix); return s; };

@@ -7,5 +7,5 @@ timeout 900 python bench.py --steps 5 --warmup 3 --no-full --no-cpu-baseline --c
 grep -E "ef=|FULL" gpurun_out/tune_${TAG}_base.log
 for EF in ${EFS:-64 128}; do for H in ${HS:-10 11 12 13}; do
   PA_HASH_LOG2=$H timeout 600 python bench.py --steps 5 --warmup 3 --ef $EF --no-full --no-cpu-baseline --cache /tmp/pa_cache > gpurun_out/tune_${TAG}_ef${EF}_h${H}.json 2>/dev/null
-  python -c "import json;d=json.load(open('gpurun_out/tune_${TAG}_ef${EF}_h${H}.json'));print('ef',$EF,'hash',$H,'qps',d['value'],'trav_ms',d['roofline']['traverse_ms'],'frac',d['roofline']['frac'],'recall',d['config']['recall_at_10_gt_sub'])"
+  python -c "import json;d=json.load(open('gpurun_out/tune_${TAG}_ef${EF}_h${H}.json'));print('ef',$EF,'hash',$H,'qps',d['value'],'kernels',d['roofline']['kernel_ms'],'frac',d['roofline']['frac'],'recall',d['config']['recall_at_10_gt_sub'])"
 done; done
