@@ -122,7 +122,10 @@ struct pa_index {
     const int32_t* h_full_nb = nullptr;
     const float* h_rotated = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;                 // a7 handoff (D2H of candidates)
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> pipe_done, pipe_copied;    // per sub-batch (stages ②③ pipeline)
+    cudaEvent_t pipe_start = nullptr, pipe_end = nullptr;
     std::mutex mu;
     pa_stats stats{};
     bool events_pending = false;
@@ -234,17 +237,19 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r) {
 // Enqueue a1..a6 on stream s for device queries q → out ids/dists.
 pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k, const Resolved& r,
                             int32_t* d_out_ids, float* d_out_d, const pa_debug* dbg, bool want_qres,
-                            cudaStream_t s) {
-    pa_status st = ensure_ws(ix, m, r.E, r.ef1, k);
+                            cudaStream_t s, int64_t row0 = 0) {
+    pa_status st = ensure_ws(ix, row0 + m, r.E, r.ef1, k);
     if (st != PA_OK) return st;
+    const auto& dd = ix->dev;
     pa::SearchArgs a;
     a.m = m; a.k = k; a.ef = r.ef1; a.E = r.E; a.flags = r.flags; a.hash_log2 = r.hash_log2;
-    a.q = d_q; a.qp = ix->qp; a.qres = want_qres ? ix->qres : nullptr;
-    a.cell = (dbg && dbg->cell) ? dbg->cell : ix->cell;
-    a.entries = (dbg && dbg->entries) ? dbg->entries : ix->entries;
-    a.cand_ids = (dbg && dbg->cand_ids) ? dbg->cand_ids : ix->cand_ids;
-    a.cand_d = (dbg && dbg->cand_dists) ? dbg->cand_dists : ix->cand_d;
-    a.counters = (dbg && dbg->counters) ? dbg->counters : ix->counters;
+    a.q = d_q; a.qp = ix->qp + row0 * dd.rdim_pad;
+    a.qres = want_qres ? ix->qres + row0 * std::max(1, dd.dim - dd.rdim) : nullptr;
+    a.cell = (dbg && dbg->cell) ? dbg->cell : ix->cell + row0;
+    a.entries = (dbg && dbg->entries) ? dbg->entries : ix->entries + row0 * r.E;
+    a.cand_ids = (dbg && dbg->cand_ids) ? dbg->cand_ids : ix->cand_ids + row0 * r.ef1;
+    a.cand_d = (dbg && dbg->cand_dists) ? dbg->cand_dists : ix->cand_d + row0 * r.ef1;
+    a.counters = (dbg && dbg->counters) ? dbg->counters : ix->counters + row0 * 4;
     a.out_ids = d_out_ids; a.out_d = d_out_d;
     a.work = ix->work;
     a.perm = ix->perm; a.qoff = ix->qoff; a.toff = ix->toff; a.fes_scores = ix->fes_scores;
@@ -305,6 +310,21 @@ void collect_event_times(pa_index* ix) {
     cudaEventElapsedTime(&t03, ix->ev[0], ix->ev[3]);
     ix->stats.ms_project = t01; ix->stats.ms_fes = t12; ix->stats.ms_traverse = t23; ix->stats.ms_total_gpu = t03;
     ix->events_pending = false;
+}
+
+pa_status ensure_pipe_events(pa_index* ix, int64_t nb) {
+    while ((int64_t)ix->pipe_done.size() < nb) {
+        cudaEvent_t a, b;
+        CU(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        ix->pipe_done.push_back(a);
+        ix->pipe_copied.push_back(b);
+    }
+    if (!ix->pipe_start) {
+        CU(cudaEventCreate(&ix->pipe_start));
+        CU(cudaEventCreate(&ix->pipe_end));
+    }
+    return PA_OK;
 }
 
 pa_status ensure_host_ws(pa_index* ix, int64_t m, int32_t ef) {
@@ -434,6 +454,7 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
                              cudaGetErrorString(e_)));                                             \
     } while (0)
     CUB(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+    CUB(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
     for (auto& e : ix->ev) CUB(cudaEventCreate(&e));
     CUB(dalloc(&d.basis, (size_t)D * D));
     CUB(cudaMemcpy(d.basis, p->basis, sizeof(float) * D * D, cudaMemcpyHostToDevice));
@@ -566,10 +587,19 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
     pa_status st = ensure_ws(ix, m, r.E, r.ef1, k);
     if (st != PA_OK) return st;
     const auto& d = ix->dev;
-    CU(cudaMemcpyAsync(ix->q, queries, sizeof(float) * m * d.dim, cudaMemcpyHostToDevice, s));
-    st = enqueue_gpu_stage(ix, ix->q, m, k, r, ix->out_ids, ix->out_d, nullptr, full, s);
+    // Stages ②③ pipeline over sub-batches (GPU stage of batch j+1 overlaps host work on j).
+    const int64_t bsz = full ? std::max<int64_t>(1024, (m + 7) / 8) : m;
+    const int64_t nb = (m + bsz - 1) / bsz;
+    if (full) {
+        st = ensure_pipe_events(ix, nb);
+        if (st != PA_OK) return st;
+        CU(cudaEventRecord(ix->pipe_start, s));
+    }
+    const int64_t m0 = std::min(m, bsz);
+    CU(cudaMemcpyAsync(ix->q, queries, sizeof(float) * m0 * d.dim, cudaMemcpyHostToDevice, s));
+    st = enqueue_gpu_stage(ix, ix->q, m0, k, r, ix->out_ids, ix->out_d, nullptr, full, s);
     if (st != PA_OK) return st;
-    const int64_t launches = ix->stats.kernel_launches;
+    int64_t launches = ix->stats.kernel_launches;
     if (candidates_only) {
         CU(cudaMemcpyAsync(out_ids, ix->cand_ids, sizeof(int32_t) * m * r.ef1, cudaMemcpyDeviceToHost, s));
         CU(cudaMemcpyAsync(out_d, ix->cand_d, sizeof(float) * m * r.ef1, cudaMemcpyDeviceToHost, s));
@@ -581,27 +611,65 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
     } else {
         st = ensure_host_ws(ix, m, r.ef1);
         if (st != PA_OK) return st;
-        CU(cudaMemcpyAsync(ix->h_cand_ids, ix->cand_ids, sizeof(int32_t) * m * r.ef1, cudaMemcpyDeviceToHost, s));
-        CU(cudaMemcpyAsync(ix->h_cand_d, ix->cand_d, sizeof(float) * m * r.ef1, cudaMemcpyDeviceToHost, s));
-        CU(cudaMemcpyAsync(ix->h_qp, ix->qp, sizeof(float) * m * d.rdim_pad, cudaMemcpyDeviceToHost, s));
-        if (d.dim > d.rdim)
-            CU(cudaMemcpyAsync(ix->h_qres, ix->qres, sizeof(float) * m * (d.dim - d.rdim), cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-        auto th = std::chrono::steady_clock::now();
-        pa::HostStageArgs h;
-        h.dim = d.dim; h.rdim = d.rdim; h.metric = d.metric;
-        h.sub.off = ix->h_sub_off.data(); h.sub.nb = ix->h_sub_nb.data();
-        h.full.off = ix->h_full_off; h.full.nb = ix->h_full_nb;
-        h.rotated = ix->h_rotated;
-        h.m = m; h.k = k; h.ef1 = r.ef1; h.ef2 = r.ef2; h.ef3 = r.ef3; h.refine_iters = r.refine;
-        h.flags = r.flags; h.threads = r.threads;
-        h.cand_ids = ix->h_cand_ids; h.cand_d = ix->h_cand_d; h.qp = ix->h_qp; h.qp_stride = d.rdim_pad;
-        h.qres = ix->h_qres; h.out_ids = out_ids; h.out_d = out_d;
+        // The first sub-batch was enqueued above; the rest are enqueued now so the
+        // GPU stage of batch j+1.. runs while the host refines batch j (A12).
+        std::vector<int64_t> lo(nb + 1);
+        for (int64_t j = 0; j <= nb; ++j) lo[j] = std::min<int64_t>(m, j * bsz);
+        for (int64_t j = 0; j < nb; ++j) {
+            const int64_t a0 = lo[j], mj = lo[j + 1] - lo[j];
+            if (j > 0) {
+                CU(cudaMemcpyAsync(ix->q + a0 * d.dim, queries + a0 * d.dim, sizeof(float) * mj * d.dim,
+                                   cudaMemcpyHostToDevice, s));
+                st = enqueue_gpu_stage(ix, ix->q + a0 * d.dim, mj, k, r, ix->out_ids + a0 * k, ix->out_d + a0 * k,
+                                       nullptr, true, s, a0);
+                if (st != PA_OK) return st;
+                launches += ix->stats.kernel_launches;
+            }
+            CU(cudaEventRecord(ix->pipe_done[j], s));
+            CU(cudaStreamWaitEvent(ix->copy_stream, ix->pipe_done[j], 0));
+            cudaStream_t c = ix->copy_stream;
+            CU(cudaMemcpyAsync(ix->h_cand_ids + a0 * r.ef1, ix->cand_ids + a0 * r.ef1, sizeof(int32_t) * mj * r.ef1,
+                               cudaMemcpyDeviceToHost, c));
+            CU(cudaMemcpyAsync(ix->h_cand_d + a0 * r.ef1, ix->cand_d + a0 * r.ef1, sizeof(float) * mj * r.ef1,
+                               cudaMemcpyDeviceToHost, c));
+            CU(cudaMemcpyAsync(ix->h_qp + a0 * d.rdim_pad, ix->qp + a0 * d.rdim_pad, sizeof(float) * mj * d.rdim_pad,
+                               cudaMemcpyDeviceToHost, c));
+            if (d.dim > d.rdim)
+                CU(cudaMemcpyAsync(ix->h_qres + a0 * (d.dim - d.rdim), ix->qres + a0 * (d.dim - d.rdim),
+                                   sizeof(float) * mj * (d.dim - d.rdim), cudaMemcpyDeviceToHost, c));
+            CU(cudaEventRecord(ix->pipe_copied[j], c));
+        }
+        CU(cudaEventRecord(ix->pipe_end, s));
+        double host_ms = 0;
         int64_t s2 = 0, s3 = 0;
-        h.sum_n_dist2 = &s2; h.sum_n_dist3 = &s3;
-        pa::run_host_stages(h);
-        ix->stats.ms_host_stages = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th).count();
+        for (int64_t j = 0; j < nb; ++j) {
+            const int64_t a0 = lo[j], mj = lo[j + 1] - lo[j];
+            CU(cudaEventSynchronize(ix->pipe_copied[j]));
+            auto th = std::chrono::steady_clock::now();
+            pa::HostStageArgs h;
+            h.dim = d.dim; h.rdim = d.rdim; h.metric = d.metric;
+            h.sub.off = ix->h_sub_off.data(); h.sub.nb = ix->h_sub_nb.data();
+            h.full.off = ix->h_full_off; h.full.nb = ix->h_full_nb;
+            h.rotated = ix->h_rotated;
+            h.m = mj; h.k = k; h.ef1 = r.ef1; h.ef2 = r.ef2; h.ef3 = r.ef3; h.refine_iters = r.refine;
+            h.flags = r.flags; h.threads = r.threads;
+            h.cand_ids = ix->h_cand_ids + a0 * r.ef1; h.cand_d = ix->h_cand_d + a0 * r.ef1;
+            h.qp = ix->h_qp + a0 * d.rdim_pad; h.qp_stride = d.rdim_pad;
+            h.qres = ix->h_qres + a0 * std::max(1, d.dim - d.rdim);
+            h.out_ids = out_ids + a0 * k; h.out_d = out_d + a0 * k;
+            h.sum_n_dist2 = &s2; h.sum_n_dist3 = &s3;
+            pa::run_host_stages(h);
+            host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th).count();
+        }
+        CU(cudaStreamSynchronize(s));
+        float gpu_ms = 0;
+        cudaEventElapsedTime(&gpu_ms, ix->pipe_start, ix->pipe_end);
+        ix->stats = pa_stats{};
+        ix->stats.queries = m;
+        ix->stats.ms_total_gpu = gpu_ms;
+        ix->stats.ms_host_stages = host_ms;
         ix->stats.sum_n_dist2 = s2; ix->stats.sum_n_dist3 = s3;
+        ix->events_pending = false;
     }
     collect_event_times(ix);
     ix->stats.kernel_launches = launches;
@@ -669,6 +737,7 @@ void pa_destroy(pa_index* ix) {
     }
     cudaSetDevice(ix->device);
     if (ix->stream) cudaStreamSynchronize(ix->stream);
+    if (ix->copy_stream) cudaStreamSynchronize(ix->copy_stream);
     free_ws(ix);
     cudaFree(ix->spill);
     cudaFreeHost(ix->h_cand_ids); cudaFreeHost(ix->h_cand_d); cudaFreeHost(ix->h_qp); cudaFreeHost(ix->h_qres);
@@ -677,7 +746,12 @@ void pa_destroy(pa_index* ix) {
     cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
     cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
+    for (auto e : ix->pipe_done) cudaEventDestroy(e);
+    for (auto e : ix->pipe_copied) cudaEventDestroy(e);
+    if (ix->pipe_start) cudaEventDestroy(ix->pipe_start);
+    if (ix->pipe_end) cudaEventDestroy(ix->pipe_end);
     if (ix->stream) cudaStreamDestroy(ix->stream);
+    if (ix->copy_stream) cudaStreamDestroy(ix->copy_stream);
     ix->magic = 0;
     delete ix;
 }

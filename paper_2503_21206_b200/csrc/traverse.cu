@@ -151,10 +151,18 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
             return isnew;
         };
         // δ' for the new ids (l.8) and rank-merge of the keys that beat C's worst (l.9, l.11).
-        auto merge_batch = [&](int32_t v, bool isnew) {
-            if (__ballot_sync(kFull, isnew) == 0) return;
+        uint64_t minnew = kKeyInf;     // smallest new key of the current expansion
+        auto merge_batch = [&](int32_t v, bool isnew, auto&& before_merge) {
+            if (__ballot_sync(kFull, isnew) == 0) { before_merge(); return; }
             uint64_t key = kKeyInf;
             if (isnew) key = make_key(row_dist<METRIC>(qs, ix.reduced + (int64_t)v * dps, dps), v);
+            {
+                const uint32_t hi = __reduce_min_sync(kFull, (uint32_t)(key >> 32));
+                const uint32_t lo = __reduce_min_sync(kFull, (uint32_t)(key >> 32) == hi ? (uint32_t)key : 0xffffffffu);
+                const uint64_t mk = ((uint64_t)hi << 32) | lo;
+                minnew = mk < minnew ? mk : minnew;
+            }
+            before_merge();
             const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
             const bool pass = key < thresh;                   // unique keys: strict
             const unsigned pb = __ballot_sync(kFull, pass);
@@ -169,7 +177,7 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
             const int j = j0 + lane;
             const int32_t v = j < a.E ? a.entries[q * a.E + j] : -1;
             const bool isnew = visit_batch(v);
-            if (status == 0) merge_batch(v, isnew);
+            if (status == 0) merge_batch(v, isnew, [] {});
         }
         // ---- a6: Alg 1 l.4-12.  Speculation: the runner-up unchecked node u2 is
         // the likely next expansion; its ELL row is loaded into registers (sv)
@@ -207,13 +215,15 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
 #pragma unroll
                     for (int c = 0; c < ELLW / 32; ++c) vv[c] = __ldg(row + c * 32 + lane);
                 }
-                const int32_t u2 = p2 >= 0 ? key_id(C[p2]) : -1;
-                if (u2 >= 0) {
+                const uint64_t key_p2 = p2 >= 0 ? C[p2] : kKeyInf;
+                const int32_t u2 = p2 >= 0 ? key_id(key_p2) : -1;
+                if (u2 >= 0 && u2 != u) {
                     const int32_t* row2 = ix.ell + (int64_t)u2 * ELLW;
 #pragma unroll
                     for (int c = 0; c < ELLW / 32; ++c) sv[c] = __ldg(row2 + c * 32 + lane);
                 }
-                spec_u = u2;
+                spec_u = u2 != u ? u2 : -1;
+                minnew = kKeyInf;
                 __syncwarp();
                 if (lane == 0) C[p] = ku | 1ull;                    // mark checked
                 hint = p + 1;
@@ -232,7 +242,20 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
                                 prefetch_row_l2(ix.reduced + (int64_t)w2 * dps, dps * 4);
                         }
                     }
-                    if (status == 0) merge_batch(vv[c], isnew);
+                    if (status == 0)
+                        merge_batch(vv[c], isnew, [&] {
+                            // The next expansion is exactly min(runner-up, best new key): issue its
+                            // ELL row now so the load overlaps this merge (Alg 1 l.5 of the next step).
+                            if (c != ELLW / 32 - 1) return;
+                            const uint64_t nk = minnew < key_p2 ? minnew : key_p2;
+                            if (nk == kKeyInf) return;
+                            const int32_t nu = key_id(nk);
+                            if (nu == spec_u) return;
+                            const int32_t* rown = ix.ell + (int64_t)nu * ELLW;
+#pragma unroll
+                            for (int c3 = 0; c3 < ELLW / 32; ++c3) sv[c3] = __ldg(rown + c3 * 32 + lane);
+                            spec_u = nu;
+                        });
                 }
                 if (it >= kIterCap) status = 2;
             }
