@@ -154,6 +154,35 @@ __device__ __forceinline__ float row_dist(const float* __restrict__ qs, const fl
     return METRIC == 0 ? s : -s;
 }
 
+// Same, with the row length a compile-time number of float4s: every load of the
+// row is issued before the first FMA (one DRAM round trip per row instead of
+// one per unroll group); DPS4 == 0 falls back to the runtime loop.
+template <int METRIC, int DPS4>
+__device__ __forceinline__ float row_dist_t(const float* __restrict__ qs, const float* __restrict__ x, int dps) {
+    if constexpr (DPS4 == 0) {
+        return row_dist<METRIC>(qs, x, dps);
+    } else {
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* q4 = reinterpret_cast<const float4*>(qs);
+        float4 v[DPS4];
+#pragma unroll
+        for (int i = 0; i < DPS4; ++i) v[i] = __ldg(x4 + i);
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int i = 0; i < DPS4; ++i) {
+            const float4 w = q4[i];
+            if (METRIC == 0) {
+                const float d0 = v[i].x - w.x, d1 = v[i].y - w.y, d2 = v[i].z - w.z, d3 = v[i].w - w.w;
+                a0 = fmaf(d0, d0, a0); a1 = fmaf(d1, d1, a1); a2 = fmaf(d2, d2, a2); a3 = fmaf(d3, d3, a3);
+            } else {
+                a0 = fmaf(v[i].x, w.x, a0); a1 = fmaf(v[i].y, w.y, a1); a2 = fmaf(v[i].z, w.z, a2); a3 = fmaf(v[i].w, w.w, a3);
+            }
+        }
+        const float s = (a0 + a1) + (a2 + a3);
+        return METRIC == 0 ? s : -s;
+    }
+}
+
 __device__ __forceinline__ uint64_t warp_min64(uint64_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

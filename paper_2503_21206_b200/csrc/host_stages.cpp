@@ -61,13 +61,24 @@ struct VisitedSet {
     }
 };
 
-inline float dist_full(const float* q, const float* x, int d, int metric) {
-    float s = 0.f;
+// 16 independent partial sums so the compiler emits packed FMAs (AVX2/AVX-512)
+// without -ffast-math; the tail runs scalar.
+inline float dist_full(const float* __restrict__ q, const float* __restrict__ x, int d, int metric) {
+    float acc[16] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int i = 0;
     if (metric == 0) {
-        for (int i = 0; i < d; ++i) { float t = q[i] - x[i]; s += t * t; }
+        for (; i + 16 <= d; i += 16)
+            for (int j = 0; j < 16; ++j) { const float t = q[i + j] - x[i + j]; acc[j] += t * t; }
+        float s = 0.f;
+        for (int j = 0; j < 16; ++j) s += acc[j];
+        for (; i < d; ++i) { const float t = q[i] - x[i]; s += t * t; }
         return s;
     }
-    for (int i = 0; i < d; ++i) s += q[i] * x[i];
+    for (; i + 16 <= d; i += 16)
+        for (int j = 0; j < 16; ++j) acc[j] += q[i + j] * x[i + j];
+    float s = 0.f;
+    for (int j = 0; j < 16; ++j) s += acc[j];
+    for (; i < d; ++i) s += q[i] * x[i];
     return -s;
 }
 
@@ -113,6 +124,7 @@ void run_host_stages(const HostStageArgs& a) {
         for (;;) {
             const int64_t q = next.fetch_add(1);
             if (q >= a.m) break;
+            if (a.wait_ready) a.wait_ready(a.ready_ctx, q);
             std::memcpy(qh.data(), a.qp + q * a.qp_stride, sizeof(float) * dp);
             if (dr > 0) std::memcpy(qh.data() + dp, a.qres + q * dr, sizeof(float) * dr);
             auto dfull = [&](int32_t v) { return dist_full(qh.data(), a.rotated + (int64_t)v * D, D, a.metric); };

@@ -27,6 +27,11 @@ struct HostStageArgs {
     float* out_d = nullptr;             // [m][k]
     int64_t* sum_n_dist2 = nullptr;
     int64_t* sum_n_dist3 = nullptr;
+    // Optional pipelining hook: called before a worker first touches a query of a
+    // new sub-batch (queries are claimed in increasing order), e.g. to wait for the
+    // D2H of that sub-batch's candidates.
+    void (*wait_ready)(void* ctx, int64_t q) = nullptr;
+    void* ready_ctx = nullptr;
 };
 
 void run_host_stages(const HostStageArgs& a);

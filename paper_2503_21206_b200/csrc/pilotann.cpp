@@ -105,7 +105,7 @@ int default_hash_log2(int ef) {
         int v = std::atoi(e);
         if (v >= 5 && v <= 15) return v;
     }
-    return ef <= 64 ? 11 : 12;
+    return ef <= 128 ? 11 : 12;
 }
 
 }  // namespace
@@ -640,27 +640,39 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
             CU(cudaEventRecord(ix->pipe_copied[j], c));
         }
         CU(cudaEventRecord(ix->pipe_end, s));
-        double host_ms = 0;
+        // One pass of the host worker pool over all m queries; a worker entering a
+        // new sub-batch waits for that sub-batch's D2H event only.
+        struct Ready {
+            pa_index* ix;
+            int64_t bsz;
+            std::vector<std::atomic<int>> done;
+            explicit Ready(size_t n) : done(n) {}
+        } ready(nb);
+        ready.ix = ix;
+        ready.bsz = bsz;
+        for (auto& x : ready.done) x.store(0);
+        auto th = std::chrono::steady_clock::now();
+        pa::HostStageArgs h;
+        h.dim = d.dim; h.rdim = d.rdim; h.metric = d.metric;
+        h.sub.off = ix->h_sub_off.data(); h.sub.nb = ix->h_sub_nb.data();
+        h.full.off = ix->h_full_off; h.full.nb = ix->h_full_nb;
+        h.rotated = ix->h_rotated;
+        h.m = m; h.k = k; h.ef1 = r.ef1; h.ef2 = r.ef2; h.ef3 = r.ef3; h.refine_iters = r.refine;
+        h.flags = r.flags; h.threads = r.threads;
+        h.cand_ids = ix->h_cand_ids; h.cand_d = ix->h_cand_d; h.qp = ix->h_qp; h.qp_stride = d.rdim_pad;
+        h.qres = ix->h_qres; h.out_ids = out_ids; h.out_d = out_d;
         int64_t s2 = 0, s3 = 0;
-        for (int64_t j = 0; j < nb; ++j) {
-            const int64_t a0 = lo[j], mj = lo[j + 1] - lo[j];
-            CU(cudaEventSynchronize(ix->pipe_copied[j]));
-            auto th = std::chrono::steady_clock::now();
-            pa::HostStageArgs h;
-            h.dim = d.dim; h.rdim = d.rdim; h.metric = d.metric;
-            h.sub.off = ix->h_sub_off.data(); h.sub.nb = ix->h_sub_nb.data();
-            h.full.off = ix->h_full_off; h.full.nb = ix->h_full_nb;
-            h.rotated = ix->h_rotated;
-            h.m = mj; h.k = k; h.ef1 = r.ef1; h.ef2 = r.ef2; h.ef3 = r.ef3; h.refine_iters = r.refine;
-            h.flags = r.flags; h.threads = r.threads;
-            h.cand_ids = ix->h_cand_ids + a0 * r.ef1; h.cand_d = ix->h_cand_d + a0 * r.ef1;
-            h.qp = ix->h_qp + a0 * d.rdim_pad; h.qp_stride = d.rdim_pad;
-            h.qres = ix->h_qres + a0 * std::max(1, d.dim - d.rdim);
-            h.out_ids = out_ids + a0 * k; h.out_d = out_d + a0 * k;
-            h.sum_n_dist2 = &s2; h.sum_n_dist3 = &s3;
-            pa::run_host_stages(h);
-            host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th).count();
-        }
+        h.sum_n_dist2 = &s2; h.sum_n_dist3 = &s3;
+        h.ready_ctx = &ready;
+        h.wait_ready = [](void* ctx, int64_t q) {
+            Ready* R = static_cast<Ready*>(ctx);
+            const int64_t j = q / R->bsz;
+            if (R->done[j].load(std::memory_order_acquire)) return;
+            cudaEventSynchronize(R->ix->pipe_copied[j]);
+            R->done[j].store(1, std::memory_order_release);
+        };
+        pa::run_host_stages(h);
+        const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th).count();
         CU(cudaStreamSynchronize(s));
         float gpu_ms = 0;
         cudaEventElapsedTime(&gpu_ms, ix->pipe_start, ix->pipe_end);

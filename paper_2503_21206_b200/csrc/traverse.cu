@@ -95,8 +95,9 @@ __device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
     return false;
 }
 
-template <int METRIC, int ELLW, int SMAX, bool TRACE>
-__global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArgs a) {
+template <int METRIC, int ELLW, int SMAX, int DPS4>
+__global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArgs a) {
+    const bool TRACE = a.trace_cap > 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
         auto merge_batch = [&](int32_t v, bool isnew, auto&& before_merge) {
             if (__ballot_sync(kFull, isnew) == 0) { before_merge(); return; }
             uint64_t key = kKeyInf;
-            if (isnew) key = make_key(row_dist<METRIC>(qs, ix.reduced + (int64_t)v * dps, dps), v);
+            if (isnew) key = make_key(row_dist_t<METRIC, DPS4>(qs, ix.reduced + (int64_t)v * dps, dps), v);
             {
                 const uint32_t hi = __reduce_min_sync(kFull, (uint32_t)(key >> 32));
                 const uint32_t lo = __reduce_min_sync(kFull, (uint32_t)(key >> 32) == hi ? (uint32_t)key : 0xffffffffu);
@@ -284,18 +285,23 @@ __global__ void __launch_bounds__(kTW * 32, 8) k_traverse(DevIndex ix, SearchArg
 }
 
 template <int METRIC, int ELLW, int SMAX>
-void* pick3(bool trace) {
-    return trace ? (void*)k_traverse<METRIC, ELLW, SMAX, true> : (void*)k_traverse<METRIC, ELLW, SMAX, false>;
+void* pick4(int dps) {
+    switch (dps) {
+        case 32: return (void*)k_traverse<METRIC, ELLW, SMAX, 8>;
+        case 48: return (void*)k_traverse<METRIC, ELLW, SMAX, 12>;
+        case 64: return (void*)k_traverse<METRIC, ELLW, SMAX, 16>;
+        default: return (void*)k_traverse<METRIC, ELLW, SMAX, 0>;
+    }
 }
 template <int METRIC, int ELLW>
-void* pick2(int ef, bool trace) {
-    if (ef <= 64) return pick3<METRIC, ELLW, 2>(trace);
-    if (ef <= 128) return pick3<METRIC, ELLW, 4>(trace);
-    return pick3<METRIC, ELLW, 8>(trace);
+void* pick2(int ef, int dps) {
+    if (ef <= 64) return pick4<METRIC, ELLW, 2>(dps);
+    if (ef <= 128) return pick4<METRIC, ELLW, 4>(dps);
+    return pick4<METRIC, ELLW, 8>(dps);
 }
-void* pick(int metric, int ellw, int ef, bool trace) {
-    if (metric == 0) return ellw == 32 ? pick2<0, 32>(ef, trace) : pick2<0, 64>(ef, trace);
-    return ellw == 32 ? pick2<1, 32>(ef, trace) : pick2<1, 64>(ef, trace);
+void* pick(int metric, int ellw, int ef, int dps) {
+    if (metric == 0) return ellw == 32 ? pick2<0, 32>(ef, dps) : pick2<0, 64>(ef, dps);
+    return ellw == 32 ? pick2<1, 32>(ef, dps) : pick2<1, 64>(ef, dps);
 }
 
 size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
@@ -306,7 +312,7 @@ size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
 }  // namespace
 
 int traverse_max_warps(const DevIndex& ix, const SearchArgs& a) {
-    void* fn = pick(ix.metric, ix.ell_w, a.ef, a.trace_cap > 0);
+    void* fn = pick(ix.metric, ix.ell_w, a.ef, ix.rdim_pad);
     size_t smem = smem_bytes(ix, a);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = 0, dev = 0, sms = 0;
@@ -319,7 +325,7 @@ int traverse_max_warps(const DevIndex& ix, const SearchArgs& a) {
 
 int launch_traverse(const DevIndex& ix, const SearchArgs& a, int grid_warps, cudaStream_t s) {
     if (a.m == 0) return 0;
-    void* fn = pick(ix.metric, ix.ell_w, a.ef, a.trace_cap > 0);
+    void* fn = pick(ix.metric, ix.ell_w, a.ef, ix.rdim_pad);
     size_t smem = smem_bytes(ix, a);
     int64_t want = (a.m + kTW - 1) / kTW;
     int64_t blocks = grid_warps / kTW;

@@ -13,7 +13,7 @@ fi
 timeout 1500 python bench.py ${BENCH_ARGS:---steps 10 --warmup 3} --cache /tmp/pa_cache > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.log; echo "bench rc $?"
 if [ -z "$SKIP_NCU" ]; then
 EF=$(python -c "import json;print(json.load(open('gpurun_out/bench_$TAG.json'))['config']['ef'])" 2>/dev/null || echo 32)
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_(project|fes|traverse)' --csv \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(project|fes|traverse|bucket)" --csv \
    --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --ef $EF --no-full --no-cpu-baseline --cache /tmp/pa_cache \
    > gpurun_out/ncu_launch_bench.log 2>&1; echo "ncu launches rc $?"
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_traverse -s 4 -c 1 \
