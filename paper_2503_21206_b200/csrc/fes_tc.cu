@@ -15,6 +15,8 @@
 // Every GEMM tile is dense (cell-centric tiling, Table 3 density mn/(r(m+n)),
 // P:L417).
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "internal.h"
@@ -95,6 +97,8 @@ struct FesParams {
     const int32_t* pool_ids;
     const int32_t* cell_off;
     int metric;
+    const float* pool_img;       // [chunks][kch][hi,lo][4096] pre-split, pre-swizzled B tiles (TMA source)
+    const int32_t* chunk_off;    // [r+1] first 128-entry chunk of each cell
     float* scores;               // [m][sstride] GEMM-form scores, row = bucketed position
     int sstride;                 // ≥ max cell size, multiple of 4
     int E;
@@ -214,6 +218,144 @@ __global__ void __launch_bounds__(kThreads, 1) k_fes_scores(FesParams p) {
     }
 }
 
+// Same GEMM, warp-specialised and pipelined: warp 4 (one elected thread) streams
+// the cell's pre-split, pre-swizzled pool tiles with 1-D TMA bulk copies into a
+// 2-stage smem ring (full/empty mbarriers) and issues the tcgen05.mma; the
+// accumulator is double-buffered in TMEM (2 × 128 columns, ready/free
+// mbarriers) so warps 0-3 drain chunk j (tcgen05.ld → scores) while the tensor
+// core works on chunk j+1.
+template <int METRIC>
+__global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int t = blockIdx.x;
+    if (t >= p.toff[p.r]) return;
+    int c = 0;
+    while (c + 1 < p.r && p.toff[c + 1] <= t) ++c;
+    const int pos0 = p.qoff[c] + (t - p.toff[c]) * kM;
+    const int nrows = min(kM, p.qoff[c + 1] - pos0);
+    const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
+    const int kch = p.kchunks;
+    const int nchunk = (nc + kN - 1) / kN;
+    const int S = nchunk * kch;
+    const float* img = p.pool_img + (size_t)p.chunk_off[c] * kch * 2 * 4096;
+
+    unsigned char* a_hi = smem;                               // kch × 16 KB
+    unsigned char* a_lo = a_hi + kch * 16384;
+    unsigned char* bst = a_lo + kch * 16384;                  // 2 stages × (hi 16 KB | lo 16 KB)
+    uint64_t* full = reinterpret_cast<uint64_t*>(bst + 2 * 32768);
+    uint64_t* empty = full + 2;
+    uint64_t* accf = empty + 2;
+    uint64_t* acce = accf + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(acce + 2);
+
+    if (warp == 0) tmem_alloc(tslot, 2 * kN);
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, 1);
+            mbar_init(accf + i, 1);
+            mbar_init(acce + i, kThreads);
+        }
+    }
+    if (warp < 4) {                                           // A: routed q' rows, hi/lo, swizzled
+        const int q = tid < nrows ? p.perm[pos0 + tid] : -1;
+        for (int kc = 0; kc < kch; ++kc) {
+#pragma unroll 8
+            for (int k = 0; k < 32; ++k) {
+                const int col = kc * 32 + k;
+                const float a = (q >= 0 && col < p.dps) ? __ldg(p.qp + (int64_t)q * p.dps + col) : 0.f;
+                float hi, lo;
+                split_tf32(a, hi, lo);
+                const uint32_t off = (uint32_t)kc * 16384 + sw128_off(tid, k);
+                *reinterpret_cast<float*>(a_hi + off) = hi;
+                *reinterpret_cast<float*>(a_lo + off) = lo;
+            }
+        }
+        fence_proxy_async();
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 4) {
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc_tf32(kM, kN);
+            auto issue = [&](int s) {
+                const int st = s & 1;
+                unsigned char* dst = bst + st * 32768;
+                const float* src = img + (size_t)s * 2 * 4096;          // step s = (chunk s/kch, kc s%kch)
+                mbar_expect_tx(full + st, 32768);
+                tma_bulk_g2s(dst, src, 16384, full + st);
+                tma_bulk_g2s(dst + 16384, src + 4096, 16384, full + st);
+            };
+            for (int s = 0; s < S && s < 2; ++s) issue(s);
+            for (int s = 0; s < S; ++s) {
+                const int st = s & 1, j = s / kch, kc = s % kch, acc = j & 1;
+                if (kc == 0 && j >= 2) mbar_wait(acce + acc, ((j >> 1) - 1) & 1);
+                mbar_wait(full + st, (s >> 1) & 1);
+                tmem_fence_after();
+                const uint32_t sah = smem_u32(a_hi) + kc * 16384, sal = smem_u32(a_lo) + kc * 16384;
+                const uint32_t sbh = smem_u32(bst + st * 32768), sbl = sbh + 16384;
+                const uint32_t td = tmem + (uint32_t)(acc * kN);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t ko = kk * 32;
+                    const uint32_t acc0 = (kc > 0 || kk > 0) ? 1u : 0u;
+                    mma_tf32(td, make_desc_sw128(sah + ko), make_desc_sw128(sbh + ko), idesc, acc0);
+                    mma_tf32(td, make_desc_sw128(sah + ko), make_desc_sw128(sbl + ko), idesc, 1u);
+                    mma_tf32(td, make_desc_sw128(sal + ko), make_desc_sw128(sbh + ko), idesc, 1u);
+                }
+                mma_commit(empty + st);
+                if (kc == kch - 1) mma_commit(accf + acc);
+                if (s + 2 < S) {
+                    mbar_wait(empty + st, (s >> 1) & 1);
+                    issue(s + 2);
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        const int row = tid;
+        float* srow = p.scores + (int64_t)(pos0 + row) * p.sstride;
+        for (int j = 0; j < nchunk; ++j) {
+            const int acc = j & 1;
+            mbar_wait(accf + acc, (j >> 1) & 1);
+            tmem_fence_after();
+            for (int c0 = 0; c0 < kN; c0 += 32) {
+                float v[32];
+                tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * kN + c0), v);
+                const int jb = j * kN + c0;
+                if (row < nrows && jb < nc) {
+#pragma unroll
+                    for (int jj = 0; jj < 32; jj += 4) {
+                        float4 o;
+                        float* op = &o.x;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int col = jb + jj + u;
+                            op[u] = METRIC == 0 ? fmaf(-2.f, v[jj + u], col < nc ? __ldg(p.pool_norm + pb + col) : 0.f)
+                                                : -v[jj + u];
+                        }
+                        if (jb + jj < nc) *reinterpret_cast<float4*>(srow + jb + jj) = o;
+                    }
+                }
+            }
+            tmem_fence_before();
+            mbar_arrive(acce + acc);
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tmem_fence_after();
+        tmem_dealloc(tmem, 2 * kN);
+    }
+}
+
+size_t fes_scores_tma_smem(int kch) { return (size_t)kch * 2 * 16384 + 2 * 32768 + 8 * 8 + 16; }
+
 // Selection: one warp per bucketed query — E smallest (score, pool id) keys over
 // its cell's scores, kept sorted by the same threshold filter + rank merge as
 // the traversal (common.cuh).
@@ -267,12 +409,21 @@ int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
     p.perm = a.perm; p.qoff = a.qoff; p.toff = a.toff; p.r = ix.fes_r;
     p.pool_vec = ix.pool_vec; p.pool_norm = ix.pool_norm; p.pool_ids = ix.pool_ids; p.cell_off = ix.cell_off;
     p.metric = ix.metric; p.scores = a.fes_scores; p.sstride = ix.max_cell; p.E = a.E; p.entries = a.entries;
-    const size_t smem = fes_scores_smem(p.kchunks);
+    p.pool_img = ix.pool_img; p.chunk_off = ix.chunk_off;
     const unsigned grid = (unsigned)((a.m + kM - 1) / kM + ix.fes_r);
-    void* fn = ix.metric == 0 ? (void*)k_fes_scores<0> : (void*)k_fes_scores<1>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     void* args[] = {&p};
-    cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
+    const char* ke = std::getenv("PA_FES_SCORES");
+    if (ix.pool_img && !(ke && !std::strcmp(ke, "plain"))) {
+        const size_t smem = fes_scores_tma_smem(p.kchunks);
+        void* fn = ix.metric == 0 ? (void*)k_fes_scores_tma<0> : (void*)k_fes_scores_tma<1>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaLaunchKernel(fn, dim3(grid), dim3(160), args, smem, s);
+    } else {
+        const size_t smem = fes_scores_smem(p.kchunks);
+        void* fn = ix.metric == 0 ? (void*)k_fes_scores<0> : (void*)k_fes_scores<1>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
+    }
     void* sel = a.E <= 64 ? (void*)k_fes_select<2> : a.E <= 128 ? (void*)k_fes_select<4> : (void*)k_fes_select<8>;
     const size_t ssm = (size_t)4 * a.E * 8;
     cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);

@@ -24,6 +24,9 @@ struct DevIndex {
     float* cent_norm = nullptr;                // [r] ‖centroid‖²
     float* pool_norm = nullptr;                // [pool_n] ‖e‖² (GEMM-form FES scores)
     int32_t max_cell = 0;                      // largest FES cell (score scratch row stride, multiple of 4)
+    float* pool_img = nullptr;                 // [chunks][kch][hi,lo][4096]: pool split to TF32 hi/lo and laid
+                                               // out as K-major SWIZZLE_128B 128×32 tiles (TMA bulk sources)
+    int32_t* chunk_off = nullptr;              // [r+1] first 128-entry pool chunk of each cell
 };
 
 struct SearchArgs {

@@ -512,6 +512,43 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
         }
         CUB(dalloc(&d.pool_norm, pn.size()));
         CUB(cudaMemcpy(d.pool_norm, pn.data(), sizeof(float) * pn.size(), cudaMemcpyHostToDevice));
+        // Pre-split, pre-swizzled pool tiles for the TMA-fed tcgen05 FES GEMM:
+        // per cell, per 128-entry chunk, per 32-float K chunk: hi tile then lo tile,
+        // element (row, k) at the K-major SWIZZLE_128B offset used by the kernel.
+        const int kch = (dps + 31) / 32;
+        std::vector<int32_t> choff(r + 1, 0);
+        for (int c = 0; c < r; ++c)
+            choff[c + 1] = choff[c] + (int32_t)((p->fes_cell_off[c + 1] - p->fes_cell_off[c] + 127) / 128);
+        std::vector<float> img((size_t)choff[r] * kch * 2 * 4096, 0.f);
+        auto swz = [](int row, int k) {
+            return (size_t)((row >> 3) * 256 + (row & 7) * 32 + (((k >> 2) ^ (row & 7)) << 2) + (k & 3));
+        };
+        for (int c = 0; c < r; ++c) {
+            const int64_t b = p->fes_cell_off[c], nc = p->fes_cell_off[c + 1] - b;
+            for (int64_t e = 0; e < nc; ++e) {
+                const int ch = choff[c] + (int)(e / 128), row = (int)(e % 128);
+                const float* src = p->reduced + (int64_t)p->fes_pool_ids[b + e] * dp;
+                for (int kc = 0; kc < kch; ++kc) {
+                    float* hi = &img[(((size_t)ch * kch + kc) * 2 + 0) * 4096];
+                    float* lo = &img[(((size_t)ch * kch + kc) * 2 + 1) * 4096];
+                    for (int k = 0; k < 32; ++k) {
+                        const int col = kc * 32 + k;
+                        const float a = col < dp ? src[col] : 0.f;
+                        uint32_t bits;
+                        std::memcpy(&bits, &a, 4);
+                        bits &= 0xFFFFE000u;
+                        float h;
+                        std::memcpy(&h, &bits, 4);
+                        hi[swz(row, k)] = h;
+                        lo[swz(row, k)] = a - h;
+                    }
+                }
+            }
+        }
+        CUB(dalloc(&d.pool_img, img.size()));
+        CUB(cudaMemcpy(d.pool_img, img.data(), sizeof(float) * img.size(), cudaMemcpyHostToDevice));
+        CUB(dalloc(&d.chunk_off, choff.size()));
+        CUB(cudaMemcpy(d.chunk_off, choff.data(), sizeof(int32_t) * choff.size(), cudaMemcpyHostToDevice));
     }
     // tcgen05 projection operand B_T = [(V_{:d'}·Cᵀ)ᵀ ; Vᵀ] (rows K-major), fp64 → fp32, zero-padded
     {
@@ -757,6 +794,7 @@ void pa_destroy(pa_index* ix) {
     auto& d = ix->dev;
     cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
     cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
+    cudaFree(d.pool_img); cudaFree(d.chunk_off);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
     for (auto e : ix->pipe_done) cudaEventDestroy(e);
     for (auto e : ix->pipe_copied) cudaEventDestroy(e);
