@@ -214,7 +214,7 @@ def csr_from_rows(rows: np.ndarray, N: int, ids: Optional[np.ndarray] = None):
 
 
 def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, labels=None,
-              metric: str = "l2", P: int = 0, chunk: int = 4096, refine: int = int(__import__("os").environ.get("PA_KNN_REFINE", "0"))):
+              metric: str = "l2", P: int = 0, chunk: int = 4096, refine: int = -1):
     """Degree-R kNN graph over the rows `ids` of X (all rows if None), neighbour
     lists in ascending-distance order, self excluded.  Exact brute force when
     `labels` is None; otherwise candidates are restricted to the P nearest
@@ -240,7 +240,7 @@ def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, label
         return out
     lab = labels[ids]
     Kc = int(labels.max().item()) + 1
-    P = P or int(__import__("os").environ.get("PA_KNN_P", "32"))
+    P = P or int(__import__("os").environ.get("PA_KNN_P", "64"))
     order = torch.argsort(lab, stable=True)
     counts = torch.bincount(lab, minlength=Kc)
     starts = torch.zeros(Kc + 1, dtype=torch.int64, device=dev)
@@ -269,7 +269,9 @@ def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, label
         v, jj = torch.topk(d, kk, dim=1, largest=False)
         g = torch.where(torch.isfinite(v), ids[cand[jj]], torch.full_like(jj, -1))
         out[a, :kk] = g
-    if refine:
+    if refine < 0:          # default: one neighbour-of-neighbour pass above 200K rows (graph_quality.py:
+        refine = int(__import__("os").environ.get("PA_KNN_REFINE", "1" if n > 200_000 else "0"))
+    if refine:              # 10M, P=64: 10-NN accuracy 0.745 → 0.894)
         out = refine_knn(X, out, ids, iters=refine)
     return out
 

@@ -7,8 +7,9 @@
 //              smem; lane l owns positions l, l+32, ... during a merge.
 //   visited  : EXACT set (Alg 1's "unvisited" test, I4) — level 1 = open-addressing
 //              int32 hash in smem (2^hash_log2 slots, accepts inserts while ≤ half
-//              full); level 2 = per-warp epoch-tagged 64-bit hash slab in global
-//              memory once level 1 closes.  The paper's bloom filter
+//              full); level 2 = per-warp open-addressing slab in global memory
+//              (one atomicCAS per probe, used slots logged and zeroed at the end of
+//              the query) once level 1 closes.  The paper's bloom filter
 //              is NEXT-f1.
 //   loop     : u ← smallest unchecked key (ballot scan from a "all checked before"
 //              hint, Alg 1 l.5); the runner-up's ELL row is prefetched into L2;
@@ -35,14 +36,14 @@ struct Visited {
     volatile int32_t* H;   // smem level 1
     int log2S;
     int count1;            // entries in level 1 (warp-uniform)
-    uint64_t* G;           // global level 2 slab
+    uint32_t* G;           // global level 2 slab: 2^L slots (0 = empty, else id+1) ...
+    uint32_t* log;         // ... followed by the log of slots used by the current query
     uint32_t gmask;
-    uint32_t epoch;
     int count2;            // entries in level 2 (warp-uniform)
 };
 
 // Returns true iff v was not yet visited (and is now).  `open1` is warp-uniform.
-__device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& in_l2) {
+__device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& in_l2, uint32_t& slot) {
     in_l2 = false;
     const uint32_t S = 1u << vs.log2S;
     uint32_t h = hash1(v) >> (32 - vs.log2S);
@@ -57,21 +58,14 @@ __device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& 
         }
         h = (h + 1) & (S - 1);
     }
-    // level 2: epoch-tagged slots; a slot whose epoch differs is free
-    const uint64_t tag = ((uint64_t)vs.epoch << 32) | (uint32_t)v;
+    // level 2: one atomicCAS per probe (empty slots are 0; the query's used slots
+    // are logged and zeroed when it finishes, so no epoch tags are needed)
+    const uint32_t tag = (uint32_t)v + 1u;
     uint32_t g = hash2(v) & vs.gmask;
     for (uint32_t p = 0; p <= vs.gmask; ++p) {
-        uint64_t cur = *(volatile uint64_t*)&vs.G[g];
-        while (true) {
-            if ((uint32_t)(cur >> 32) == vs.epoch) {
-                if ((uint32_t)cur == (uint32_t)v) return false;
-                break;
-            }
-            unsigned long long old = atomicCAS((unsigned long long*)&vs.G[g], (unsigned long long)cur,
-                                               (unsigned long long)tag);
-            if (old == cur) { in_l2 = true; return true; }
-            cur = old;
-        }
+        const uint32_t old = atomicCAS(&vs.G[g], 0u, tag);
+        if (old == 0u) { in_l2 = true; slot = g; return true; }
+        if (old == tag) return false;
         g = (g + 1) & vs.gmask;
     }
     return false;   // unreachable while count2 ≤ gmask/2 (guarded by the caller)
@@ -113,7 +107,8 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
     Visited vs;
     vs.H = H;
     vs.log2S = a.hash_log2;
-    vs.G = a.spill + ((int64_t)gw << a.spill_log2);
+    vs.G = reinterpret_cast<uint32_t*>(a.spill + ((int64_t)gw << a.spill_log2));   // 8 B × 2^L per warp
+    vs.log = vs.G + ((size_t)1 << a.spill_log2);                                    // slots: 4 B × 2^L, log after
     vs.gmask = (1u << a.spill_log2) - 1u;
     const int cap1 = S >> 1, cap2 = (int)(vs.gmask >> 1);
 
@@ -122,7 +117,6 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
         if (lane == 0) q = atomicAdd(a.work, 1);
         q = __shfl_sync(kFull, (int)q, 0);
         if (q >= a.m) break;
-        vs.epoch = a.epoch_base + (uint32_t)q;
         vs.count1 = 0;
         vs.count2 = 0;
         for (int i = lane; i < dps; i += 32) qs[i] = a.qp[q * dps + i];
@@ -138,10 +132,12 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
             const bool open1 = vs.count1 + 32 <= cap1;
             if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
             bool l2 = false;
-            const bool isnew = v >= 0 && visit(vs, v, open1, l2);
+            uint32_t slot = 0;
+            const bool isnew = v >= 0 && visit(vs, v, open1, l2, slot);
             const unsigned bal = __ballot_sync(kFull, isnew);
             const unsigned bl2 = __ballot_sync(kFull, l2);
             const int nnew = __popc(bal);
+            if (l2) vs.log[vs.count2 + __popc(bl2 & lt_mask)] = slot;
             if (open1) vs.count1 += nnew; else vs.count2 += __popc(bl2);
             n_spill += __popc(bl2);
             if (TRACE && isnew) {
@@ -273,6 +269,8 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
             a.out_ids[q * a.k + i] = i < csz ? key_id(C[i]) : -1;
             a.out_d[q * a.k + i] = i < csz ? key_dist(C[i]) : inf;
         }
+        for (int i = lane; i < vs.count2; i += 32) vs.G[vs.log[i]] = 0u;   // reset the level-2 slots used
+        __syncwarp();
         if (lane == 0) {
             if (a.counters) {
                 int4 c4 = make_int4(n_exp, n_dist, n_spill, status);

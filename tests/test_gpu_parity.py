@@ -190,3 +190,27 @@ def test_tensor_core_paths_match_simt(cfg_name, request, monkeypatch):
     same = np.array([set(a) == set(b) for a, b in zip(tc["entries"], si["entries"])])
     assert same.mean() >= 0.95, same.mean()
     assert orc.recall(tc["ids"], si["ids"], cfg.k) >= 0.97
+
+
+@pytest.mark.parametrize("cfg_name", ["C0", "S1", "S2"])
+def test_full_pipeline_parity(cfg_name, request):
+    """PA_STAGES_FULL (GPU stage ① + host stages ②③, pipelined) vs the oracle's
+    three stages in fp64: full-space recall@10 within 0.002 of the oracle's against
+    the same exhaustive ground truth; returned distances = fp64 full δ."""
+    inst = request.getfixturevalue(cfg_name.lower())
+    cfg = inst["cfg"]
+    ix = pa.Index.from_instance(inst)
+    ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
+    ids, d = ix.search(inst["queries"], k=cfg.k, ef=cfg.ef, stages=pa.PA_STAGES_FULL)
+    st = ix.stats()
+    ix.close()
+    r = orc.search(inst, k=cfg.k, ef=cfg.ef, stages=3)
+    gt = inst["gt_ids"][:, :cfg.k]
+    rg, ro = orc.recall(ids, gt, cfg.k), orc.recall(r["ids"], gt, cfg.k)
+    print(cfg_name, "full recall gpu+host", rg, "oracle", ro, "host ms", st["ms_host_stages"])
+    assert abs(rg - ro) <= 0.002 + 1e-12
+    Qh = orc.project(inst["queries"], inst["basis"])
+    X = inst["rotated"].astype(np.float64)[ids]
+    want = ((X - Qh[:, None, :]) ** 2).sum(2) if cfg.metric == "l2" else -(X * Qh[:, None, :]).sum(2)
+    scale = np.abs(want) if cfg.metric == "l2" else np.abs(X * Qh[:, None, :]).sum(2)
+    assert np.all(np.abs(d - want) <= 1e-5 * scale + 1e-6 * np.sqrt(np.abs(want) * (Qh ** 2).sum(1, keepdims=True)))
