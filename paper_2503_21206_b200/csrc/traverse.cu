@@ -20,6 +20,9 @@
 //              passing key the warp counts, with one shuffle and ef/32 ballots,
 //              its rank in C and its shift of C's entries; everything moves in
 //              place (registers hold the old C across one __syncwarp).
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -42,21 +45,49 @@ struct Visited {
     int count2;            // entries in level 2 (warp-uniform)
 };
 
+// Compact level 1 (ids < 2^24, ≥ 2^11 slots): 16-bit slots.  The id is mapped by
+// a bijection P on 24 bits; the top log2S bits of P(v) are its home slot and the
+// slot stores the remaining 24−log2S bits with the displacement d ≤ 6 from home
+// (quotienting), so (slot, stored value) identifies v exactly.  0xFFFF = empty.
+// A full 7-slot window sends v to level 2 (lookups follow the same rule, so an
+// id is in level 2 only if its window was full when it was inserted).
+__device__ __forceinline__ uint32_t perm24(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) & 0xFFFFFFu; }
+
 // Returns true iff v was not yet visited (and is now).  `open1` is warp-uniform.
+template <bool COMPACT>
 __device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& in_l2, uint32_t& slot) {
     in_l2 = false;
     const uint32_t S = 1u << vs.log2S;
-    uint32_t h = hash1(v) >> (32 - vs.log2S);
-    for (uint32_t p = 0; p < S; ++p) {
-        int32_t cur = vs.H[h];
-        if (cur == v) return false;
-        if (cur == -1) {
-            if (!open1) break;                                   // not in level 1
-            int32_t old = atomicCAS((int32_t*)&vs.H[h], -1, v);
-            if (old == -1) return true;
-            if (old == v) return false;
+    if constexpr (COMPACT) {
+        volatile uint16_t* H16 = reinterpret_cast<volatile uint16_t*>(vs.H);
+        const uint32_t P = perm24(v);
+        const uint32_t home = P >> (24 - vs.log2S);
+        const uint32_t rem = P & ((1u << (24 - vs.log2S)) - 1u);
+        for (uint32_t d = 0; d < 7; ++d) {
+            const uint32_t h = (home + d) & (S - 1);
+            const uint16_t want = (uint16_t)((rem << 3) | d);
+            const uint16_t cur = H16[h];
+            if (cur == want) return false;
+            if (cur == 0xFFFFu) {
+                if (!open1) break;                               // not in level 1
+                const unsigned short old = atomicCAS((unsigned short*)&H16[h], (unsigned short)0xFFFFu, want);
+                if (old == 0xFFFFu) return true;
+                if (old == want) return false;
+            }
         }
-        h = (h + 1) & (S - 1);
+    } else {
+        uint32_t h = hash1(v) >> (32 - vs.log2S);
+        for (uint32_t p = 0; p < S; ++p) {
+            int32_t cur = vs.H[h];
+            if (cur == v) return false;
+            if (cur == -1) {
+                if (!open1) break;                               // not in level 1
+                int32_t old = atomicCAS((int32_t*)&vs.H[h], -1, v);
+                if (old == -1) return true;
+                if (old == v) return false;
+            }
+            h = (h + 1) & (S - 1);
+        }
     }
     // level 2: one atomicCAS per probe (empty slots are 0; the query's used slots
     // are logged and zeroed when it finishes, so no epoch tags are needed)
@@ -77,8 +108,21 @@ __device__ __forceinline__ void prefetch_row_l2(const void* p, int bytes) {
 }
 
 // Lookup-only probe of the level-1 hash (speculation; false negatives only cost a prefetch).
+template <bool COMPACT>
 __device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
     const uint32_t S = 1u << vs.log2S;
+    if constexpr (COMPACT) {
+        const volatile uint16_t* H16 = reinterpret_cast<const volatile uint16_t*>(vs.H);
+        const uint32_t P = perm24(v);
+        const uint32_t home = P >> (24 - vs.log2S);
+        const uint32_t rem = P & ((1u << (24 - vs.log2S)) - 1u);
+        for (uint32_t d = 0; d < 7; ++d) {
+            const uint16_t cur = H16[(home + d) & (S - 1)];
+            if (cur == (uint16_t)((rem << 3) | d)) return true;
+            if (cur == 0xFFFFu) return false;
+        }
+        return false;
+    }
     uint32_t h = hash1(v) >> (32 - vs.log2S);
     for (uint32_t p = 0; p < 8; ++p) {
         const int32_t cur = vs.H[h];
@@ -89,14 +133,15 @@ __device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
     return false;
 }
 
-template <int METRIC, int ELLW, int SMAX, int DPS4>
+template <int METRIC, bool COMPACT, int SMAX, int DPS4>
 __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArgs a) {
     const bool TRACE = a.trace_cap > 0;
+    const int ELLW = ix.ell_w, NCH = ix.ell_w >> 5;         // ELL row width 32 or 64
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
     const int efp = (ef + 1) & ~1;                      // keep qs 16-B aligned
-    const size_t per_warp = (size_t)efp * 8 + (size_t)dps * 4 + (size_t)S * 4;
+    const size_t per_warp = (size_t)efp * 8 + (size_t)dps * 4 + (size_t)S * (COMPACT ? 2 : 4);
     unsigned char* base = smem_raw + per_warp * w;
     uint64_t* C = reinterpret_cast<uint64_t*>(base);
     float* qs = reinterpret_cast<float*>(C + efp);
@@ -121,7 +166,7 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
         vs.count2 = 0;
         for (int i = lane; i < dps; i += 32) qs[i] = a.qp[q * dps + i];
         int4* H4 = reinterpret_cast<int4*>(H);
-        for (int i = lane; i < (S >> 2); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
+        for (int i = lane; i < (S >> (COMPACT ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
         __syncwarp();
 
         int csz = 0, hint = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
@@ -133,12 +178,13 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
             if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
             bool l2 = false;
             uint32_t slot = 0;
-            const bool isnew = v >= 0 && visit(vs, v, open1, l2, slot);
+            const bool isnew = v >= 0 && visit<COMPACT>(vs, v, open1, l2, slot);
             const unsigned bal = __ballot_sync(kFull, isnew);
             const unsigned bl2 = __ballot_sync(kFull, l2);
             const int nnew = __popc(bal);
             if (l2) vs.log[vs.count2 + __popc(bl2 & lt_mask)] = slot;
-            if (open1) vs.count1 += nnew; else vs.count2 += __popc(bl2);
+            vs.count1 += nnew - __popc(bl2);
+            vs.count2 += __popc(bl2);
             n_spill += __popc(bl2);
             if (TRACE && isnew) {
                 int pos = n_dist + __popc(bal & lt_mask);
@@ -183,9 +229,7 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
         // guess makes the next iteration's two dependent loads L2 hits; a wrong
         // guess only costs bandwidth.  The algorithm's decisions are unchanged.
         int32_t spec_u = -1;
-        int32_t sv[ELLW / 32];
-#pragma unroll
-        for (int c = 0; c < ELLW / 32; ++c) sv[c] = -1;
+        int32_t sv[2] = {-1, -1};
         if (!(a.flags & 4u)) {
             for (int it = 0; status == 0; ++it) {
                 int p = -1, p2 = -1;
@@ -203,21 +247,21 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
                 if (p < 0) break;                                   // l.12: no unchecked node
                 const uint64_t ku = C[p];
                 const int32_t u = key_id(ku);
-                int32_t vv[ELLW / 32];
+                int32_t vv[2] = {-1, -1};
                 if (u == spec_u) {
-#pragma unroll
-                    for (int c = 0; c < ELLW / 32; ++c) vv[c] = sv[c];
+                    vv[0] = sv[0];
+                    vv[1] = sv[1];
                 } else {
                     const int32_t* row = ix.ell + (int64_t)u * ELLW;
-#pragma unroll
-                    for (int c = 0; c < ELLW / 32; ++c) vv[c] = __ldg(row + c * 32 + lane);
+                    vv[0] = __ldg(row + lane);
+                    if (NCH > 1) vv[1] = __ldg(row + 32 + lane);
                 }
                 const uint64_t key_p2 = p2 >= 0 ? C[p2] : kKeyInf;
                 const int32_t u2 = p2 >= 0 ? key_id(key_p2) : -1;
                 if (u2 >= 0 && u2 != u) {
                     const int32_t* row2 = ix.ell + (int64_t)u2 * ELLW;
-#pragma unroll
-                    for (int c = 0; c < ELLW / 32; ++c) sv[c] = __ldg(row2 + c * 32 + lane);
+                    sv[0] = __ldg(row2 + lane);
+                    sv[1] = NCH > 1 ? __ldg(row2 + 32 + lane) : -1;
                 }
                 spec_u = u2 != u ? u2 : -1;
                 minnew = kKeyInf;
@@ -228,14 +272,14 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
                 ++n_exp;
                 __syncwarp();
 #pragma unroll
-                for (int c = 0; c < ELLW / 32; ++c) {
-                    if (status != 0) break;
+                for (int c = 0; c < 2; ++c) {
+                    if (c >= NCH || status != 0) break;
                     const bool isnew = visit_batch(vv[c]);
                     if (c == 0 && u2 >= 0) {
 #pragma unroll
-                        for (int c2 = 0; c2 < ELLW / 32; ++c2) {
+                        for (int c2 = 0; c2 < 2; ++c2) {
                             const int32_t w2 = sv[c2];
-                            if (w2 >= 0 && !visited_l1(vs, w2))
+                            if (w2 >= 0 && !visited_l1<COMPACT>(vs, w2))
                                 prefetch_row_l2(ix.reduced + (int64_t)w2 * dps, dps * 4);
                         }
                     }
@@ -243,14 +287,14 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
                         merge_batch(vv[c], isnew, [&] {
                             // The next expansion is exactly min(runner-up, best new key): issue its
                             // ELL row now so the load overlaps this merge (Alg 1 l.5 of the next step).
-                            if (c != ELLW / 32 - 1) return;
+                            if (c != NCH - 1) return;
                             const uint64_t nk = minnew < key_p2 ? minnew : key_p2;
                             if (nk == kKeyInf) return;
                             const int32_t nu = key_id(nk);
                             if (nu == spec_u) return;
                             const int32_t* rown = ix.ell + (int64_t)nu * ELLW;
-#pragma unroll
-                            for (int c3 = 0; c3 < ELLW / 32; ++c3) sv[c3] = __ldg(rown + c3 * 32 + lane);
+                            sv[0] = __ldg(rown + lane);
+                            sv[1] = NCH > 1 ? __ldg(rown + 32 + lane) : -1;
                             spec_u = nu;
                         });
                 }
@@ -282,35 +326,41 @@ __global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArg
     }
 }
 
-template <int METRIC, int ELLW, int SMAX>
+template <int METRIC, bool COMPACT, int SMAX>
 void* pick4(int dps) {
     switch (dps) {
-        case 32: return (void*)k_traverse<METRIC, ELLW, SMAX, 8>;
-        case 48: return (void*)k_traverse<METRIC, ELLW, SMAX, 12>;
-        case 64: return (void*)k_traverse<METRIC, ELLW, SMAX, 16>;
-        default: return (void*)k_traverse<METRIC, ELLW, SMAX, 0>;
+        case 32: return (void*)k_traverse<METRIC, COMPACT, SMAX, 8>;
+        case 48: return (void*)k_traverse<METRIC, COMPACT, SMAX, 12>;
+        case 64: return (void*)k_traverse<METRIC, COMPACT, SMAX, 16>;
+        default: return (void*)k_traverse<METRIC, COMPACT, SMAX, 0>;
     }
 }
-template <int METRIC, int ELLW>
+template <int METRIC, bool COMPACT>
 void* pick2(int ef, int dps) {
-    if (ef <= 64) return pick4<METRIC, ELLW, 2>(dps);
-    if (ef <= 128) return pick4<METRIC, ELLW, 4>(dps);
-    return pick4<METRIC, ELLW, 8>(dps);
+    if (ef <= 64) return pick4<METRIC, COMPACT, 2>(dps);
+    if (ef <= 128) return pick4<METRIC, COMPACT, 4>(dps);
+    return pick4<METRIC, COMPACT, 8>(dps);
 }
-void* pick(int metric, int ellw, int ef, int dps) {
-    if (metric == 0) return ellw == 32 ? pick2<0, 32>(ef, dps) : pick2<0, 64>(ef, dps);
-    return ellw == 32 ? pick2<1, 32>(ef, dps) : pick2<1, 64>(ef, dps);
+bool use_compact(const DevIndex& ix, const SearchArgs& a) {
+    const char* e = std::getenv("PA_VISITED");
+    if (e && !std::strcmp(e, "wide")) return false;
+    return ix.n <= (1 << 24) && a.hash_log2 >= 11 && a.hash_log2 <= 13;
+}
+void* pick(const DevIndex& ix, const SearchArgs& a) {
+    const bool cp = use_compact(ix, a);
+    if (ix.metric == 0) return cp ? pick2<0, true>(a.ef, ix.rdim_pad) : pick2<0, false>(a.ef, ix.rdim_pad);
+    return cp ? pick2<1, true>(a.ef, ix.rdim_pad) : pick2<1, false>(a.ef, ix.rdim_pad);
 }
 
 size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
     const size_t efp = (size_t)((a.ef + 1) & ~1);
-    size_t per_warp = efp * 8 + (size_t)ix.rdim_pad * 4 + ((size_t)4 << a.hash_log2);
+    size_t per_warp = efp * 8 + (size_t)ix.rdim_pad * 4 + ((size_t)(use_compact(ix, a) ? 2 : 4) << a.hash_log2);
     return per_warp * kTW;
 }
 }  // namespace
 
 int traverse_max_warps(const DevIndex& ix, const SearchArgs& a) {
-    void* fn = pick(ix.metric, ix.ell_w, a.ef, ix.rdim_pad);
+    void* fn = pick(ix, a);
     size_t smem = smem_bytes(ix, a);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = 0, dev = 0, sms = 0;
@@ -323,7 +373,7 @@ int traverse_max_warps(const DevIndex& ix, const SearchArgs& a) {
 
 int launch_traverse(const DevIndex& ix, const SearchArgs& a, int grid_warps, cudaStream_t s) {
     if (a.m == 0) return 0;
-    void* fn = pick(ix.metric, ix.ell_w, a.ef, ix.rdim_pad);
+    void* fn = pick(ix, a);
     size_t smem = smem_bytes(ix, a);
     int64_t want = (a.m + kTW - 1) / kTW;
     int64_t blocks = grid_warps / kTW;

@@ -107,16 +107,24 @@ def test_config_parity(cfg_name, request):
     assert np.all(g["status"] == 0)
 
 
-def test_forced_spill_is_exact(s1):
+def test_forced_spill_is_exact(s1, monkeypatch):
+    """The visited set is exact whatever its layout: a small level-1 table (forced
+    global spill), the 32-bit table and the 16-bit quotiented table all give
+    bit-identical outputs, traces and counters."""
     cfg = s1["cfg"]
     ix = pa.Index.from_instance(s1)
     base = run_gpu(ix, s1, cfg.k, cfg.ef, trace_cap=8192)
-    for log2 in (5, 9):
-        sp = run_gpu(ix, s1, cfg.k, cfg.ef, trace_cap=8192, hash_slots_log2=log2)
-        assert sp["spill"].sum() > 0
-        for key in ("ids", "d", "cand_ids", "cand_dists", "trace_expand", "trace_visit", "n_dist1"):
-            assert np.array_equal(base[key], sp[key]), key
+    runs = [run_gpu(ix, s1, cfg.k, cfg.ef, trace_cap=8192, hash_slots_log2=log2) for log2 in (5, 9)]
+    assert all(r["spill"].sum() > 0 for r in runs)
+    runs.append(run_gpu(ix, s1, cfg.k, 256, trace_cap=8192, hash_slots_log2=11))        # compact, spills
+    monkeypatch.setenv("PA_VISITED", "wide")
+    runs.append(run_gpu(ix, s1, cfg.k, 256, trace_cap=8192, hash_slots_log2=11))        # 32-bit, spills
+    runs.append(run_gpu(ix, s1, cfg.k, cfg.ef, trace_cap=8192))
     ix.close()
+    for key in ("ids", "d", "cand_ids", "cand_dists", "trace_expand", "trace_visit", "n_dist1"):
+        for r in runs[:2] + runs[4:]:
+            assert np.array_equal(base[key], r[key]), key
+        assert np.array_equal(runs[2][key], runs[3][key]), key
 
 
 def test_edge_cases(s1):
