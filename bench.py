@@ -205,6 +205,11 @@ def run_ours(args, rank, world, local_rank):
     ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
     log(f"[rank {rank}] pa_build {time.time() - t0:.1f}s")
 
+    if args.repeat_queries > 1:      # experiment: same queries tiled R times (tail-effect probe)
+        inst = dict(inst, queries=np.tile(inst["queries"], (args.repeat_queries, 1)),
+                    gt_sub_ids=np.tile(inst["gt_sub_ids"], (args.repeat_queries, 1)),
+                    gt_ids=np.tile(inst["gt_ids"], (args.repeat_queries, 1)))
+        m = inst["queries"].shape[0]
     qd = torch.from_numpy(inst["queries"]).to(dev)
     out_i = torch.empty(m, k, dtype=torch.int32, device=dev)
     out_d = torch.empty(m, k, dtype=torch.float32, device=dev)
@@ -390,6 +395,7 @@ def main():
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cache", default=None, help="dir to cache the generated instance (same-call reuse only)")
+    ap.add_argument("--repeat-queries", type=int, default=1, help="experiment only: tile the query batch R times")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -371,10 +371,21 @@ __global__ void __launch_bounds__(128) k_fes_select(FesParams p, int64_t m) {
         while (c + 1 < p.r && p.qoff[c + 1] <= pos) ++c;
         const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
         const float* srow = p.scores + pos * p.sstride;
+        const int32_t* prow = p.pool_ids + pb;
         int csz = 0;
+        // software-pipelined: the next batch's scores and ids are loaded before the
+        // current batch is filtered / merged
+        float ns = lane < nc ? srow[lane] : 0.f;
+        int32_t ni = lane < nc ? __ldg(prow + lane) : 0;
         for (int j0 = 0; j0 < nc; j0 += 32) {
             const int j = j0 + lane;
-            const uint64_t key = j < nc ? make_key(srow[j], __ldg(p.pool_ids + pb + j)) : kKeyInf;
+            const float sc = ns;
+            const int32_t id = ni;
+            if (j + 32 < nc) {
+                ns = srow[j + 32];
+                ni = __ldg(prow + j + 32);
+            }
+            const uint64_t key = j < nc ? make_key(sc, id) : kKeyInf;
             const uint64_t thresh = csz == E ? C[E - 1] : kKeyInf;
             const bool pass = key < thresh;
             const unsigned pbal = __ballot_sync(kFull, pass);

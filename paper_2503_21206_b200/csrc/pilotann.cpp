@@ -100,11 +100,15 @@ pa_status check_csr(const int64_t* off, const int32_t* nb, int64_t n, int32_t ma
     return PA_OK;
 }
 
-int default_hash_log2(int ef) {
+// Level-1 visited-table size (slots = 2^this).  Tuned on C1 (gpurun t2/t3):
+// 16-bit quotiented slots (ids < 2^24): 2^11 up to ef 64, 2^12 above (8 KB);
+// 32-bit slots: 2^11 up to ef 128 (8 KB), 2^12 above.
+int default_hash_log2(int ef, int64_t n) {
     if (const char* e = std::getenv("PA_HASH_LOG2")) {
         int v = std::atoi(e);
         if (v >= 5 && v <= 15) return v;
     }
+    if (n <= (1 << 24)) return ef <= 64 ? 11 : 12;
     return ef <= 128 ? 11 : 12;
 }
 
@@ -209,7 +213,7 @@ struct Resolved {
     uint32_t flags;
 };
 
-pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r) {
+pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, int64_t n) {
     pa_search_opts z{};
     if (!o) o = &z;
     r->stages = o->stages ? o->stages : PA_STAGES_GPU;
@@ -223,7 +227,7 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r) {
     r->width = o->width ? o->width : 1;
     r->refine = o->refine_iters == 0 ? 2 : (o->refine_iters < 0 ? 0 : o->refine_iters);
     r->flags = o->flags;
-    r->hash_log2 = o->hash_slots_log2 ? o->hash_slots_log2 : default_hash_log2(r->ef1);
+    r->hash_log2 = o->hash_slots_log2 ? o->hash_slots_log2 : default_hash_log2(r->ef1, n);
     r->threads = threads_default(o->host_threads);
     if (r->ef1 > 256 || r->ef2 > 256 || r->ef3 > 256) return fail(PA_EINVAL, "ef > 256");
     if (r->ef1 < 1 || r->ef2 < 1 || r->ef3 < 1 || r->E < 1 || r->E > 1024) return fail(PA_EINVAL, "bad ef/entries");
@@ -603,7 +607,7 @@ pa_status pa_search_device(pa_index* ix, const float* d_queries, int64_t m, int3
     if (m < 0) return fail(PA_EINVAL, "m < 0");
     if (m > 0 && (!d_queries || !d_out_ids || !d_out_dists)) return fail(PA_EINVAL, "null argument");
     Resolved r;
-    pa_status st = resolve(opts, k, ef, &r);
+    pa_status st = resolve(opts, k, ef, &r, ix->dev.n);
     if (st != PA_OK) return st;
     if (r.stages != PA_STAGES_GPU) return fail(PA_EINVAL, "pa_search_device runs stage 1 only");
     std::lock_guard<std::mutex> g(ix->mu);
@@ -733,7 +737,7 @@ pa_status pa_search(pa_index* ix, const float* queries, int64_t m, int32_t k, in
     if (m < 0) return fail(PA_EINVAL, "m < 0");
     if (m > 0 && (!queries || !out_ids || !out_dists)) return fail(PA_EINVAL, "null argument");
     Resolved r;
-    pa_status st = resolve(opts, k, ef, &r);
+    pa_status st = resolve(opts, k, ef, &r, ix->dev.n);
     if (st != PA_OK) return st;
     std::lock_guard<std::mutex> g(ix->mu);
     if (m == 0) return PA_OK;
@@ -747,7 +751,7 @@ pa_status pa_search_candidates(pa_index* ix, const float* queries, int64_t m, in
     if (m < 0) return fail(PA_EINVAL, "m < 0");
     if (m > 0 && (!queries || !cand_ids || !cand_dists)) return fail(PA_EINVAL, "null argument");
     Resolved r;
-    pa_status st = resolve(opts, 1, ef, &r);
+    pa_status st = resolve(opts, 1, ef, &r, ix->dev.n);
     if (st != PA_OK) return st;
     if (opts && opts->ef1 && opts->ef1 != ef) return fail(PA_EINVAL, "candidates are [m][ef]: ef1 must equal ef");
     std::lock_guard<std::mutex> g(ix->mu);
