@@ -146,7 +146,7 @@ def run_reference(args, rank, world):
     import oracle as orc
     orc.build()
     torch.cuda.set_device(0) if torch.cuda.is_available() else None
-    cfg, inst = make_instance(args.config, 1, 0, args.m) if torch.cuda.is_available() else make_cpu_instance(args)
+    cfg, inst = make_instance(args.config, 1, 0, args.m, args.cache) if torch.cuda.is_available() else make_cpu_instance(args)
     cores = os.cpu_count()
     sample = args.ref_sample
     Q = inst["queries"]
