@@ -83,6 +83,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def ncu_traffic(workload, ef, kernel="k_traverse"):
+    """DRAM bytes per launch of `kernel` from a committed `ncu --set full` capture
+    (profiles/ncu_traffic.json), when one exists for this workload and ef."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(workload, {}).get(str(ef))
+        return (e["dram_bytes"], e["source"]) if e and e.get("kernel") == kernel else (None, None)
+    except (OSError, ValueError, KeyError):
+        return None, None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -303,6 +316,7 @@ def run_ours(args, rank, world, local_rank):
 
     peak, peak_src = measured_peaks()
     achieved = bytes_alg / (trav / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(cfg.name, ef)
     line = None
     if rank == 0:
         cpu = None if args.no_cpu_baseline else cpu_baseline(inst, cfg, ef, args)
@@ -319,7 +333,8 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"query-sharded x{world}, replicated index"},
             "ef_sweep": sweep,
             "roofline": {"bound": "hbm", "kernel": "k_traverse", "achieved": round(achieved, 1),
-                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "traverse_ms": round(trav, 4), "alg_bytes_per_launch": bytes_alg,
                          "kernel_ms": {"project": round(sum(proj_ms) / len(proj_ms), 4),
                                        "fes": round(sum(fes_ms) / len(fes_ms), 4), "traverse": round(trav, 4)},

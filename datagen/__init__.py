@@ -85,6 +85,11 @@ CONFIGS = {
     # configs[4]: WIKI-shaped 100M x 768 sweep
     "C4": Config("C4-WIKI-100M", N=100_000_000, D=768, dp=128, metric="l2", ratio=0.25, m=65_536,
                  k=10, ef=64, shape="mixture", seed=2507),
+    # scaled-size measurement configs of the 100M rows (same recipe; the 100M graph tool is round 2)
+    "C2S": Config("C2S-T2I-shaped-10M", N=10_000_000, D=200, dp=64, metric="ip", ratio=0.25, m=10_000,
+                  k=10, ef=64, shape="mixture", ood_shift=0.5, seed=2515),
+    "C3S": Config("C3S-LAION-shaped-2M", N=2_000_000, D=768, dp=128, metric="l2", ratio=0.25, m=10_000,
+                  k=10, ef=64, shape="mixture", seed=2516),
     # scaled-down shaped configs used by parity tests (same recipe, oracle-sized)
     "S1": Config("S1-DEEP-shaped-20K", N=20_000, D=96, dp=48, metric="l2", ratio=0.33, m=256,
                  k=10, ef=64, shape="mixture", seed=2604),
@@ -270,7 +275,8 @@ def knn_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor] = None, label
         g = torch.where(torch.isfinite(v), ids[cand[jj]], torch.full_like(jj, -1))
         out[a, :kk] = g
     if refine < 0:          # default: one neighbour-of-neighbour pass above 200K rows (graph_quality.py:
-        refine = int(__import__("os").environ.get("PA_KNN_REFINE", "1" if n > 200_000 else "0"))
+        big = n > 200_000 and X.shape[1] <= 256             # (too many gathers at D = 768)
+        refine = int(__import__("os").environ.get("PA_KNN_REFINE", "1" if big else "0"))
     if refine:              # 10M, P=64: 10-NN accuracy 0.745 → 0.894)
         out = refine_knn(X, out, ids, iters=refine)
     return out

@@ -162,20 +162,26 @@ __device__ __forceinline__ float row_dist_t(const float* __restrict__ qs, const 
     if constexpr (DPS4 == 0) {
         return row_dist<METRIC>(qs, x, dps);
     } else {
+        // rows longer than 16 float4 (d' > 64) go in 16-float4 groups to bound registers
+        constexpr int G = DPS4 > 16 ? 16 : DPS4;
+        static_assert(DPS4 % G == 0, "row length must be a multiple of the group");
         const float4* x4 = reinterpret_cast<const float4*>(x);
         const float4* q4 = reinterpret_cast<const float4*>(qs);
-        float4 v[DPS4];
-#pragma unroll
-        for (int i = 0; i < DPS4; ++i) v[i] = __ldg(x4 + i);
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int i = 0; i < DPS4; ++i) {
-            const float4 w = q4[i];
-            if (METRIC == 0) {
-                const float d0 = v[i].x - w.x, d1 = v[i].y - w.y, d2 = v[i].z - w.z, d3 = v[i].w - w.w;
-                a0 = fmaf(d0, d0, a0); a1 = fmaf(d1, d1, a1); a2 = fmaf(d2, d2, a2); a3 = fmaf(d3, d3, a3);
-            } else {
-                a0 = fmaf(v[i].x, w.x, a0); a1 = fmaf(v[i].y, w.y, a1); a2 = fmaf(v[i].z, w.z, a2); a3 = fmaf(v[i].w, w.w, a3);
+        for (int g = 0; g < DPS4; g += G) {
+            float4 v[G];
+#pragma unroll
+            for (int i = 0; i < G; ++i) v[i] = __ldg(x4 + g + i);
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                const float4 w = q4[g + i];
+                if (METRIC == 0) {
+                    const float d0 = v[i].x - w.x, d1 = v[i].y - w.y, d2 = v[i].z - w.z, d3 = v[i].w - w.w;
+                    a0 = fmaf(d0, d0, a0); a1 = fmaf(d1, d1, a1); a2 = fmaf(d2, d2, a2); a3 = fmaf(d3, d3, a3);
+                } else {
+                    a0 = fmaf(v[i].x, w.x, a0); a1 = fmaf(v[i].y, w.y, a1); a2 = fmaf(v[i].z, w.z, a2); a3 = fmaf(v[i].w, w.w, a3);
+                }
             }
         }
         const float s = (a0 + a1) + (a2 + a3);

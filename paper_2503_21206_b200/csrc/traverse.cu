@@ -30,6 +30,9 @@ namespace pa {
 
 namespace {
 constexpr int kTW = 4;                 // warps per block
+#ifndef PA_TRAV_MINB
+#define PA_TRAV_MINB 6                 // min resident blocks per SM (register budget 65536/(128·this))
+#endif
 constexpr int kIterCap = 1000000;      // Q16 safety cap (status 2)
 
 __device__ __forceinline__ uint32_t hash1(int32_t v) { return (uint32_t)v * 0x9E3779B1u; }
@@ -134,7 +137,7 @@ __device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
 }
 
 template <int METRIC, bool COMPACT, int SMAX, int DPS4>
-__global__ void __launch_bounds__(kTW * 32, 6) k_traverse(DevIndex ix, SearchArgs a) {
+__global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix, SearchArgs a) {
     const bool TRACE = a.trace_cap > 0;
     const int ELLW = ix.ell_w, NCH = ix.ell_w >> 5;         // ELL row width 32 or 64
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -332,12 +335,14 @@ void* pick4(int dps) {
         case 32: return (void*)k_traverse<METRIC, COMPACT, SMAX, 8>;
         case 48: return (void*)k_traverse<METRIC, COMPACT, SMAX, 12>;
         case 64: return (void*)k_traverse<METRIC, COMPACT, SMAX, 16>;
+        case 128: return (void*)k_traverse<METRIC, COMPACT, SMAX, 32>;
         default: return (void*)k_traverse<METRIC, COMPACT, SMAX, 0>;
     }
 }
 template <int METRIC, bool COMPACT>
 void* pick2(int ef, int dps) {
     if (ef <= 64) return pick4<METRIC, COMPACT, 2>(dps);
+    if (ef <= 96) return pick4<METRIC, COMPACT, 3>(dps);
     if (ef <= 128) return pick4<METRIC, COMPACT, 4>(dps);
     return pick4<METRIC, COMPACT, 8>(dps);
 }
