@@ -103,18 +103,36 @@ __device__ __forceinline__ int rank_merge(uint64_t* C, int csz, int cap, uint64_
         sh[t] = 0;
     }
     const int np = __popc(pb);
-    int rn = 0;
+    int rn = 0, rc = 0;
+    minr = cap;
+    // two passing keys per step: independent shuffles overlap, and each key's rank
+    // in C is counted with SMAX ballots (no dependent binary search)
     while (pb) {
-        const int src = __ffs(pb) - 1;
+        const int s0 = __ffs(pb) - 1;
         pb &= pb - 1;
-        const uint64_t x = ((uint64_t)__shfl_sync(kFull, (uint32_t)(key >> 32), src) << 32) |
-                           __shfl_sync(kFull, (uint32_t)key, src);
+        const int s1 = pb ? __ffs(pb) - 1 : s0;
+        const bool two = pb != 0;
+        pb = two ? (pb & (pb - 1)) : pb;
+        const uint32_t h0 = __shfl_sync(kFull, (uint32_t)(key >> 32), s0);
+        const uint32_t l0 = __shfl_sync(kFull, (uint32_t)key, s0);
+        const uint32_t h1 = __shfl_sync(kFull, (uint32_t)(key >> 32), s1);
+        const uint32_t l1 = __shfl_sync(kFull, (uint32_t)key, s1);
+        const uint64_t x0 = ((uint64_t)h0 << 32) | l0;
+        const uint64_t x1 = ((uint64_t)h1 << 32) | l1;
+        int r0 = 0, r1 = 0;
 #pragma unroll
-        for (int t = 0; t < SMAX; ++t) sh[t] += (x < c[t]) ? 1 : 0;
-        rn += (x < key) ? 1 : 0;
+        for (int t = 0; t < SMAX; ++t) {
+            const bool lt0 = c[t] < x0, lt1 = c[t] < x1;
+            sh[t] += (lt0 ? 0 : 1) + ((two && !lt1) ? 1 : 0);
+            r0 += __popc(__ballot_sync(kFull, lt0));
+            r1 += __popc(__ballot_sync(kFull, lt1));
+        }
+        if (lane == s0) rc = r0;
+        if (two && lane == s1) rc = r1;
+        minr = min(minr, two ? min(r0, r1) : r0);
+        rn += (x0 < key) ? 1 : 0;
+        rn += (two && x1 < key) ? 1 : 0;
     }
-    const int rc = pass ? lower_bound_smem(C, csz, key) : cap;
-    minr = (int)__reduce_min_sync(kFull, (unsigned)rc);
     __syncwarp();
 #pragma unroll
     for (int t = 0; t < SMAX; ++t) {

@@ -1,360 +1,31 @@
-// a5 + a6 — stage ① traversal: Alg 1 over the sampled subgraph
-// with reduced vectors, one warp per query, persistent grid with a
-// global work counter.
-//
-// Per query (warp):
-//   C        : sorted list of ≤ ef 64-bit keys (ord(δ)<<32 | id<<1 | checked) in
-//              smem; lane l owns positions l, l+32, ... during a merge.
-//   visited  : EXACT set (Alg 1's "unvisited" test, I4) — level 1 = open-addressing
-//              int32 hash in smem (2^hash_log2 slots, accepts inserts while ≤ half
-//              full); level 2 = per-warp open-addressing slab in global memory
-//              (one atomicCAS per probe, used slots logged and zeroed at the end of
-//              the query) once level 1 closes.  The paper's bloom filter
-//              is NEXT-f1.
-//   loop     : u ← smallest unchecked key (ballot scan from a "all checked before"
-//              hint, Alg 1 l.5); the runner-up's ELL row is prefetched into L2;
-//              ELL[u][lane] (one coalesced 128-B row per 32 neighbours, l.6);
-//              test-and-insert visited (l.7); each new neighbour's lane gathers its
-//              reduced row (float4 loads) and computes δ' in fp32 (l.8); keys
-//              below C's current worst are merged by rank (l.9, l.11): for every
-//              passing key the warp counts, with one shuffle and ef/32 ballots,
-//              its rank in C and its shift of C's entries; everything moves in
-//              place (registers hold the old C across one __syncwarp).
+// a5 + a6 launcher: picks the k_traverse variant (traverse_kernel.cuh,
+// instantiated in traverse_inst_*.cu) and sizes the persistent grid.
 #include <cstdlib>
 #include <cstring>
 
-#include "common.cuh"
 #include "internal.h"
 
 namespace pa {
+namespace trav {
+void* traverse_pick_0c(int ef, int dps, bool trace);
+void* traverse_pick_0w(int ef, int dps, bool trace);
+void* traverse_pick_1c(int ef, int dps, bool trace);
+void* traverse_pick_1w(int ef, int dps, bool trace);
+constexpr int kTW = 4;
+}  // namespace trav
 
 namespace {
-constexpr int kTW = 4;                 // warps per block
-#ifndef PA_TRAV_MINB
-#define PA_TRAV_MINB 6                 // min resident blocks per SM (register budget 65536/(128·this))
-#endif
-constexpr int kIterCap = 1000000;      // Q16 safety cap (status 2)
+using trav::kTW;
 
-__device__ __forceinline__ uint32_t hash1(int32_t v) { return (uint32_t)v * 0x9E3779B1u; }
-__device__ __forceinline__ uint32_t hash2(int32_t v) { return ((uint32_t)v ^ 0x5bd1e995u) * 0x85EBCA77u; }
-
-struct Visited {
-    volatile int32_t* H;   // smem level 1
-    int log2S;
-    int count1;            // entries in level 1 (warp-uniform)
-    uint32_t* G;           // global level 2 slab: 2^L slots (0 = empty, else id+1) ...
-    uint32_t* log;         // ... followed by the log of slots used by the current query
-    uint32_t gmask;
-    int count2;            // entries in level 2 (warp-uniform)
-};
-
-// Compact level 1 (ids < 2^24, ≥ 2^11 slots): 16-bit slots.  The id is mapped by
-// a bijection P on 24 bits; the top log2S bits of P(v) are its home slot and the
-// slot stores the remaining 24−log2S bits with the displacement d ≤ 6 from home
-// (quotienting), so (slot, stored value) identifies v exactly.  0xFFFF = empty.
-// A full 7-slot window sends v to level 2 (lookups follow the same rule, so an
-// id is in level 2 only if its window was full when it was inserted).
-__device__ __forceinline__ uint32_t perm24(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) & 0xFFFFFFu; }
-
-// Returns true iff v was not yet visited (and is now).  `open1` is warp-uniform.
-template <bool COMPACT>
-__device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& in_l2, uint32_t& slot) {
-    in_l2 = false;
-    const uint32_t S = 1u << vs.log2S;
-    if constexpr (COMPACT) {
-        volatile uint16_t* H16 = reinterpret_cast<volatile uint16_t*>(vs.H);
-        const uint32_t P = perm24(v);
-        const uint32_t home = P >> (24 - vs.log2S);
-        const uint32_t rem = P & ((1u << (24 - vs.log2S)) - 1u);
-        for (uint32_t d = 0; d < 7; ++d) {
-            const uint32_t h = (home + d) & (S - 1);
-            const uint16_t want = (uint16_t)((rem << 3) | d);
-            const uint16_t cur = H16[h];
-            if (cur == want) return false;
-            if (cur == 0xFFFFu) {
-                if (!open1) break;                               // not in level 1
-                const unsigned short old = atomicCAS((unsigned short*)&H16[h], (unsigned short)0xFFFFu, want);
-                if (old == 0xFFFFu) return true;
-                if (old == want) return false;
-            }
-        }
-    } else {
-        uint32_t h = hash1(v) >> (32 - vs.log2S);
-        for (uint32_t p = 0; p < S; ++p) {
-            int32_t cur = vs.H[h];
-            if (cur == v) return false;
-            if (cur == -1) {
-                if (!open1) break;                               // not in level 1
-                int32_t old = atomicCAS((int32_t*)&vs.H[h], -1, v);
-                if (old == -1) return true;
-                if (old == v) return false;
-            }
-            h = (h + 1) & (S - 1);
-        }
-    }
-    // level 2: one atomicCAS per probe (empty slots are 0; the query's used slots
-    // are logged and zeroed when it finishes, so no epoch tags are needed)
-    const uint32_t tag = (uint32_t)v + 1u;
-    uint32_t g = hash2(v) & vs.gmask;
-    for (uint32_t p = 0; p <= vs.gmask; ++p) {
-        const uint32_t old = atomicCAS(&vs.G[g], 0u, tag);
-        if (old == 0u) { in_l2 = true; slot = g; return true; }
-        if (old == tag) return false;
-        g = (g + 1) & vs.gmask;
-    }
-    return false;   // unreachable while count2 ≤ gmask/2 (guarded by the caller)
-}
-
-// Bulk prefetch of one reduced-vector row into L2 (sm_90+ cp.async.bulk.prefetch).
-__device__ __forceinline__ void prefetch_row_l2(const void* p, int bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
-}
-
-// Lookup-only probe of the level-1 hash (speculation; false negatives only cost a prefetch).
-template <bool COMPACT>
-__device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
-    const uint32_t S = 1u << vs.log2S;
-    if constexpr (COMPACT) {
-        const volatile uint16_t* H16 = reinterpret_cast<const volatile uint16_t*>(vs.H);
-        const uint32_t P = perm24(v);
-        const uint32_t home = P >> (24 - vs.log2S);
-        const uint32_t rem = P & ((1u << (24 - vs.log2S)) - 1u);
-        for (uint32_t d = 0; d < 7; ++d) {
-            const uint16_t cur = H16[(home + d) & (S - 1)];
-            if (cur == (uint16_t)((rem << 3) | d)) return true;
-            if (cur == 0xFFFFu) return false;
-        }
-        return false;
-    }
-    uint32_t h = hash1(v) >> (32 - vs.log2S);
-    for (uint32_t p = 0; p < 8; ++p) {
-        const int32_t cur = vs.H[h];
-        if (cur == v) return true;
-        if (cur == -1) return false;
-        h = (h + 1) & (S - 1);
-    }
-    return false;
-}
-
-template <int METRIC, bool COMPACT, int SMAX, int DPS4>
-__global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix, SearchArgs a) {
-    const bool TRACE = a.trace_cap > 0;
-    const int ELLW = ix.ell_w, NCH = ix.ell_w >> 5;         // ELL row width 32 or 64
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
-    const int efp = (ef + 1) & ~1;                      // keep qs 16-B aligned
-    const size_t per_warp = (size_t)efp * 8 + (size_t)dps * 4 + (size_t)S * (COMPACT ? 2 : 4);
-    unsigned char* base = smem_raw + per_warp * w;
-    uint64_t* C = reinterpret_cast<uint64_t*>(base);
-    float* qs = reinterpret_cast<float*>(C + efp);
-    int32_t* H = reinterpret_cast<int32_t*>(qs + dps);
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const int64_t gw = (int64_t)blockIdx.x * kTW + w;
-
-    Visited vs;
-    vs.H = H;
-    vs.log2S = a.hash_log2;
-    vs.G = reinterpret_cast<uint32_t*>(a.spill + ((int64_t)gw << a.spill_log2));   // 8 B × 2^L per warp
-    vs.log = vs.G + ((size_t)1 << a.spill_log2);                                    // slots: 4 B × 2^L, log after
-    vs.gmask = (1u << a.spill_log2) - 1u;
-    const int cap1 = S >> 1, cap2 = (int)(vs.gmask >> 1);
-
-    for (;;) {
-        int64_t q = 0;
-        if (lane == 0) q = atomicAdd(a.work, 1);
-        q = __shfl_sync(kFull, (int)q, 0);
-        if (q >= a.m) break;
-        vs.count1 = 0;
-        vs.count2 = 0;
-        for (int i = lane; i < dps; i += 32) qs[i] = a.qp[q * dps + i];
-        int4* H4 = reinterpret_cast<int4*>(H);
-        for (int i = lane; i < (S >> (COMPACT ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
-        __syncwarp();
-
-        int csz = 0, hint = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
-
-        // Visited test-and-insert for one batch of ≤32 candidate ids (one per
-        // lane, −1 = none); returns whether this lane's id is new (Alg 1 l.6-7).
-        auto visit_batch = [&](int32_t v) -> bool {
-            const bool open1 = vs.count1 + 32 <= cap1;
-            if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
-            bool l2 = false;
-            uint32_t slot = 0;
-            const bool isnew = v >= 0 && visit<COMPACT>(vs, v, open1, l2, slot);
-            const unsigned bal = __ballot_sync(kFull, isnew);
-            const unsigned bl2 = __ballot_sync(kFull, l2);
-            const int nnew = __popc(bal);
-            if (l2) vs.log[vs.count2 + __popc(bl2 & lt_mask)] = slot;
-            vs.count1 += nnew - __popc(bl2);
-            vs.count2 += __popc(bl2);
-            n_spill += __popc(bl2);
-            if (TRACE && isnew) {
-                int pos = n_dist + __popc(bal & lt_mask);
-                if (pos < a.trace_cap) a.trace_visit[q * a.trace_cap + pos] = v;
-            }
-            n_dist += nnew;
-            return isnew;
-        };
-        // δ' for the new ids (l.8) and rank-merge of the keys that beat C's worst (l.9, l.11).
-        uint64_t minnew = kKeyInf;     // smallest new key of the current expansion
-        auto merge_batch = [&](int32_t v, bool isnew, auto&& before_merge) {
-            if (__ballot_sync(kFull, isnew) == 0) { before_merge(); return; }
-            uint64_t key = kKeyInf;
-            if (isnew) key = make_key(row_dist_t<METRIC, DPS4>(qs, ix.reduced + (int64_t)v * dps, dps), v);
-            {
-                const uint32_t hi = __reduce_min_sync(kFull, (uint32_t)(key >> 32));
-                const uint32_t lo = __reduce_min_sync(kFull, (uint32_t)(key >> 32) == hi ? (uint32_t)key : 0xffffffffu);
-                const uint64_t mk = ((uint64_t)hi << 32) | lo;
-                minnew = mk < minnew ? mk : minnew;
-            }
-            before_merge();
-            const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
-            const bool pass = key < thresh;                   // unique keys: strict
-            const unsigned pb = __ballot_sync(kFull, pass);
-            if (pb == 0) return;
-            int minr;
-            csz = rank_merge<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
-            hint = min(hint, minr);
-        };
-
-        // ---- a5: C := entries (Alg 1 l.3), visited := entries (Q15)
-        for (int j0 = 0; j0 < a.E && status == 0; j0 += 32) {
-            const int j = j0 + lane;
-            const int32_t v = j < a.E ? a.entries[q * a.E + j] : -1;
-            const bool isnew = visit_batch(v);
-            if (status == 0) merge_batch(v, isnew, [] {});
-        }
-        // ---- a6: Alg 1 l.4-12.  Speculation: the runner-up unchecked node u2 is
-        // the likely next expansion; its ELL row is loaded into registers (sv)
-        // alongside u's, and the reduced rows of its not-yet-visited neighbours
-        // are prefetched into L2 while u's distances are computed.  A correct
-        // guess makes the next iteration's two dependent loads L2 hits; a wrong
-        // guess only costs bandwidth.  The algorithm's decisions are unchanged.
-        int32_t spec_u = -1;
-        int32_t sv[2] = {-1, -1};
-        if (!(a.flags & 4u)) {
-            for (int it = 0; status == 0; ++it) {
-                int p = -1, p2 = -1;
-                for (int t = hint >> 5; t * 32 < csz; ++t) {
-                    const int i = t * 32 + lane;
-                    const bool un = i < csz && !key_checked(C[i]);
-                    const unsigned b = __ballot_sync(kFull, un);
-                    if (b) {
-                        p = t * 32 + __ffs(b) - 1;
-                        const unsigned b2 = b & (b - 1);
-                        if (b2) p2 = t * 32 + __ffs(b2) - 1;
-                        break;
-                    }
-                }
-                if (p < 0) break;                                   // l.12: no unchecked node
-                const uint64_t ku = C[p];
-                const int32_t u = key_id(ku);
-                int32_t vv[2] = {-1, -1};
-                if (u == spec_u) {
-                    vv[0] = sv[0];
-                    vv[1] = sv[1];
-                } else {
-                    const int32_t* row = ix.ell + (int64_t)u * ELLW;
-                    vv[0] = __ldg(row + lane);
-                    if (NCH > 1) vv[1] = __ldg(row + 32 + lane);
-                }
-                const uint64_t key_p2 = p2 >= 0 ? C[p2] : kKeyInf;
-                const int32_t u2 = p2 >= 0 ? key_id(key_p2) : -1;
-                if (u2 >= 0 && u2 != u) {
-                    const int32_t* row2 = ix.ell + (int64_t)u2 * ELLW;
-                    sv[0] = __ldg(row2 + lane);
-                    sv[1] = NCH > 1 ? __ldg(row2 + 32 + lane) : -1;
-                }
-                spec_u = u2 != u ? u2 : -1;
-                minnew = kKeyInf;
-                __syncwarp();
-                if (lane == 0) C[p] = ku | 1ull;                    // mark checked
-                hint = p + 1;
-                if (TRACE && lane == 0 && n_exp < a.trace_cap) a.trace_expand[q * a.trace_cap + n_exp] = u;
-                ++n_exp;
-                __syncwarp();
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    if (c >= NCH || status != 0) break;
-                    const bool isnew = visit_batch(vv[c]);
-                    if (c == 0 && u2 >= 0) {
-#pragma unroll
-                        for (int c2 = 0; c2 < 2; ++c2) {
-                            const int32_t w2 = sv[c2];
-                            if (w2 >= 0 && !visited_l1<COMPACT>(vs, w2))
-                                prefetch_row_l2(ix.reduced + (int64_t)w2 * dps, dps * 4);
-                        }
-                    }
-                    if (status == 0)
-                        merge_batch(vv[c], isnew, [&] {
-                            // The next expansion is exactly min(runner-up, best new key): issue its
-                            // ELL row now so the load overlaps this merge (Alg 1 l.5 of the next step).
-                            if (c != NCH - 1) return;
-                            const uint64_t nk = minnew < key_p2 ? minnew : key_p2;
-                            if (nk == kKeyInf) return;
-                            const int32_t nu = key_id(nk);
-                            if (nu == spec_u) return;
-                            const int32_t* rown = ix.ell + (int64_t)nu * ELLW;
-                            sv[0] = __ldg(rown + lane);
-                            sv[1] = NCH > 1 ? __ldg(rown + 32 + lane) : -1;
-                            spec_u = nu;
-                        });
-                }
-                if (it >= kIterCap) status = 2;
-            }
-        }
-        // ---- outputs (a7 candidate list + top-k)
-        const float inf = __int_as_float(0x7f800000);
-        if (a.cand_ids) {
-            for (int i = lane; i < ef; i += 32) {
-                a.cand_ids[q * ef + i] = i < csz ? key_id(C[i]) : -1;
-                a.cand_d[q * ef + i] = i < csz ? key_dist(C[i]) : inf;
-            }
-        }
-        for (int i = lane; i < a.k; i += 32) {
-            a.out_ids[q * a.k + i] = i < csz ? key_id(C[i]) : -1;
-            a.out_d[q * a.k + i] = i < csz ? key_dist(C[i]) : inf;
-        }
-        for (int i = lane; i < vs.count2; i += 32) vs.G[vs.log[i]] = 0u;   // reset the level-2 slots used
-        __syncwarp();
-        if (lane == 0) {
-            if (a.counters) {
-                int4 c4 = make_int4(n_exp, n_dist, n_spill, status);
-                reinterpret_cast<int4*>(a.counters)[q] = c4;
-            }
-            if (TRACE) { a.trace_nexp[q] = n_exp; a.trace_nvis[q] = n_dist; }
-        }
-        __syncwarp();
-    }
-}
-
-template <int METRIC, bool COMPACT, int SMAX>
-void* pick4(int dps) {
-    switch (dps) {
-        case 32: return (void*)k_traverse<METRIC, COMPACT, SMAX, 8>;
-        case 48: return (void*)k_traverse<METRIC, COMPACT, SMAX, 12>;
-        case 64: return (void*)k_traverse<METRIC, COMPACT, SMAX, 16>;
-        case 128: return (void*)k_traverse<METRIC, COMPACT, SMAX, 32>;
-        default: return (void*)k_traverse<METRIC, COMPACT, SMAX, 0>;
-    }
-}
-template <int METRIC, bool COMPACT>
-void* pick2(int ef, int dps) {
-    if (ef <= 64) return pick4<METRIC, COMPACT, 2>(dps);
-    if (ef <= 96) return pick4<METRIC, COMPACT, 3>(dps);
-    if (ef <= 128) return pick4<METRIC, COMPACT, 4>(dps);
-    return pick4<METRIC, COMPACT, 8>(dps);
-}
 bool use_compact(const DevIndex& ix, const SearchArgs& a) {
     const char* e = std::getenv("PA_VISITED");
     if (e && !std::strcmp(e, "wide")) return false;
     return ix.n <= (1 << 24) && a.hash_log2 >= 11 && a.hash_log2 <= 13;
 }
 void* pick(const DevIndex& ix, const SearchArgs& a) {
-    const bool cp = use_compact(ix, a);
-    if (ix.metric == 0) return cp ? pick2<0, true>(a.ef, ix.rdim_pad) : pick2<0, false>(a.ef, ix.rdim_pad);
-    return cp ? pick2<1, true>(a.ef, ix.rdim_pad) : pick2<1, false>(a.ef, ix.rdim_pad);
+    const bool cp = use_compact(ix, a), tr = a.trace_cap > 0;
+    if (ix.metric == 0) return cp ? trav::traverse_pick_0c(a.ef, ix.rdim_pad, tr) : trav::traverse_pick_0w(a.ef, ix.rdim_pad, tr);
+    return cp ? trav::traverse_pick_1c(a.ef, ix.rdim_pad, tr) : trav::traverse_pick_1w(a.ef, ix.rdim_pad, tr);
 }
 
 size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
