@@ -214,7 +214,7 @@ def run_ours(args, rank, world, local_rank):
     k = cfg.k
     m = inst["queries"].shape[0]
     t0 = time.time()
-    ix = pa.Index.from_instance(inst, device=local_rank)
+    ix = pa.Index.from_instance(inst, device=local_rank, reduced_fp16=args.reduced == "fp16")
     ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
     log(f"[rank {rank}] pa_build {time.time() - t0:.1f}s")
 
@@ -277,7 +277,8 @@ def run_ours(args, rank, world, local_rank):
             proj_ms.append(st["ms_project"])
             fes_ms.append(st["ms_fes"])
             launches += st["kernel_launches"]
-            bytes_alg = st["sum_n_exp"] * 4 * ell_w + st["sum_n_dist"] * 4 * cfg.dp
+            row_bytes = 2 * ((cfg.dp + 7) // 8 * 8) if args.reduced == "fp16" else 4 * cfg.dp
+            bytes_alg = st["sum_n_exp"] * 4 * ell_w + st["sum_n_dist"] * row_bytes
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -319,7 +320,8 @@ def run_ours(args, rank, world, local_rank):
     traffic, traffic_src = ncu_traffic(cfg.name, ef)
     line = None
     if rank == 0:
-        cpu = None if args.no_cpu_baseline else cpu_baseline(inst, cfg, ef, args)
+        oinst = inst if args.reduced == "fp32" else dict(inst, reduced=inst["reduced"].astype(np.float16).astype(np.float32))
+        cpu = None if args.no_cpu_baseline else cpu_baseline(oinst, cfg, ef, args)
         clocks = clk.summary()
         line = {
             "metric": "QPS at Recall@10=0.90 (GPU stage: projection+FES+subgraph traversal, GT_sub)",
@@ -330,6 +332,7 @@ def run_ours(args, rank, world, local_rank):
                        "sampling_ratio": cfg.ratio, "queries_per_gpu": m, "k": k, "ef": ef,
                        "recall_at_10_gt_sub": round(rec, 4), "recall_at_10_full_gt_gpu_only": round(rec_full, 4),
                        "l2": "flushed between steps (512 MB write), per-step CUDA events",
+                       "reduced_storage": args.reduced,
                        "parallelism": f"query-sharded x{world}, replicated index"},
             "ef_sweep": sweep,
             "roofline": {"bound": "hbm", "kernel": "k_traverse", "achieved": round(achieved, 1),
@@ -338,7 +341,8 @@ def run_ours(args, rank, world, local_rank):
                          "traverse_ms": round(trav, 4), "alg_bytes_per_launch": bytes_alg,
                          "kernel_ms": {"project": round(sum(proj_ms) / len(proj_ms), 4),
                                        "fes": round(sum(fes_ms) / len(fes_ms), 4), "traverse": round(trav, 4)},
-                         "bytes_model": "sum_q n_exp*4*ELLW + n_dist*4*d'", "peak_source": peak_src},
+                         "bytes_model": "sum_q n_exp*4*ELLW + n_dist*row_bytes (4*d' fp32 / 2*round8(d') fp16)",
+                         "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": m * cfg.D * 4,
                     "d2h_bytes_per_step": m * k * 8},
@@ -411,6 +415,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cache", default=None, help="dir to cache the generated instance (same-call reuse only)")
     ap.add_argument("--repeat-queries", type=int, default=1, help="experiment only: tile the query batch R times")
+    ap.add_argument("--reduced", default="fp32", choices=["fp32", "fp16"],
+                    help="storage of the reduced rows on the GPU (fp16 = NEXT-f1; parity on the rounded values)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

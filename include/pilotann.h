@@ -86,6 +86,10 @@ typedef struct {
     const int64_t* fes_cell_off;   /* [fes_r+1] pool offsets per cell; every cell non-empty       */
     const int32_t* fes_pool_ids;   /* [fes_cell_off[fes_r]] member ids grouped by cell */
     int32_t device;                /* CUDA device ordinal of this replica                         */
+    int32_t reduced_fp16;          /* NEXT-f1: 1 = store the reduced rows as IEEE binary16,
+                                      rounded once (RNE) at build; stage ① and the FES pool then use
+                                      exactly these rounded values (half the gather bytes); stage ②
+                                      recomputes full δ from X̂.  0 = fp32 rows (default)            */
 } pa_build_params;
 
 /* Per-call options; pass NULL for defaults.  Zero fields take defaults

@@ -45,7 +45,7 @@ class BuildParams(C.Structure):
                 ("metric", C.c_int32), ("sub_offsets", C.c_void_p), ("sub_neighbors", C.c_void_p),
                 ("member_flags", C.c_void_p), ("reduced", C.c_void_p), ("basis", C.c_void_p),
                 ("fes_r", C.c_int32), ("fes_centroids", C.c_void_p), ("fes_cell_off", C.c_void_p),
-                ("fes_pool_ids", C.c_void_p), ("device", C.c_int32)]
+                ("fes_pool_ids", C.c_void_p), ("device", C.c_int32), ("reduced_fp16", C.c_int32)]
 
 
 class SearchOpts(C.Structure):
@@ -133,7 +133,8 @@ class Index:
     """One device replica (pa_build).  Arrays are host numpy arrays (copied)."""
 
     def __init__(self, *, sub_offsets, sub_neighbors, reduced, basis, fes_centroids, fes_cell_off,
-                 fes_pool_ids, member_flags=None, metric="l2", max_degree=None, device=0, n=None):
+                 fes_pool_ids, member_flags=None, metric="l2", max_degree=None, device=0, n=None,
+                 reduced_fp16=False):
         so = _c(sub_offsets, np.int64)
         sn = _c(sub_neighbors, np.int32)
         red = _c(reduced, np.float32)
@@ -151,7 +152,7 @@ class Index:
                         sub_offsets=_ptr(so), sub_neighbors=_ptr(sn), member_flags=_ptr(mf),
                         reduced=_ptr(red), basis=_ptr(bas), fes_r=int(coff.shape[0] - 1),
                         fes_centroids=_ptr(cen), fes_cell_off=_ptr(coff), fes_pool_ids=_ptr(pool),
-                        device=int(device))
+                        device=int(device), reduced_fp16=1 if reduced_fp16 else 0)
         h = C.c_void_p()
         _check(lib().pa_build(C.byref(p), C.byref(h)))
         self._h = h
@@ -160,12 +161,12 @@ class Index:
         self._host_keep = None
 
     @classmethod
-    def from_instance(cls, inst: dict, device=0, max_degree=None):
+    def from_instance(cls, inst: dict, device=0, max_degree=None, reduced_fp16=False):
         return cls(sub_offsets=inst["sub_offsets"], sub_neighbors=inst["sub_neighbors"],
                    reduced=inst["reduced"], basis=inst["basis"], fes_centroids=inst["fes_centroids"],
                    fes_cell_off=inst["fes_cell_off"], fes_pool_ids=inst["fes_pool_ids"],
                    member_flags=inst.get("member_flags"), metric=inst.get("metric", "l2"),
-                   max_degree=max_degree, device=device)
+                   max_degree=max_degree, device=device, reduced_fp16=reduced_fp16)
 
     # -- pa_attach_host -----------------------------------------------------
     def attach_host(self, full_offsets, full_neighbors, rotated):

@@ -1,6 +1,7 @@
 // Device helpers shared by the product kernels (NOT by the oracle).
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace pa {
@@ -205,6 +206,43 @@ __device__ __forceinline__ float row_dist_t(const float* __restrict__ qs, const 
         const float s = (a0 + a1) + (a2 + a3);
         return METRIC == 0 ? s : -s;
     }
+}
+
+// Direct-form distance to a binary16-stored row (NEXT-f1: half the gather bytes).
+// Values are widened exactly to fp32; arithmetic as in row_dist_t.  NV = number of
+// 16-B vectors (8 halves each) per row, all loads in flight; NV == 0 → runtime loop.
+__device__ __forceinline__ void acc8(const uint4 u, const float4 w0, const float4 w1, int metric, float& a0, float& a1,
+                                     float& a2, float& a3) {
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+    const float2 f0 = __half22float2(h[0]), f1 = __half22float2(h[1]), f2 = __half22float2(h[2]), f3 = __half22float2(h[3]);
+    if (metric == 0) {
+        float d;
+        d = f0.x - w0.x; a0 = fmaf(d, d, a0); d = f0.y - w0.y; a1 = fmaf(d, d, a1);
+        d = f1.x - w0.z; a2 = fmaf(d, d, a2); d = f1.y - w0.w; a3 = fmaf(d, d, a3);
+        d = f2.x - w1.x; a0 = fmaf(d, d, a0); d = f2.y - w1.y; a1 = fmaf(d, d, a1);
+        d = f3.x - w1.z; a2 = fmaf(d, d, a2); d = f3.y - w1.w; a3 = fmaf(d, d, a3);
+    } else {
+        a0 = fmaf(f0.x, w0.x, a0); a1 = fmaf(f0.y, w0.y, a1); a2 = fmaf(f1.x, w0.z, a2); a3 = fmaf(f1.y, w0.w, a3);
+        a0 = fmaf(f2.x, w1.x, a0); a1 = fmaf(f2.y, w1.y, a1); a2 = fmaf(f3.x, w1.z, a2); a3 = fmaf(f3.y, w1.w, a3);
+    }
+}
+
+template <int METRIC, int NV>
+__device__ __forceinline__ float row_dist_h(const float* __restrict__ qs, const __half* __restrict__ x, int dph) {
+    const uint4* x4 = reinterpret_cast<const uint4*>(x);
+    const float4* q4 = reinterpret_cast<const float4*>(qs);
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    if constexpr (NV == 0) {
+        for (int i = 0; i < (dph >> 3); ++i) acc8(__ldg(x4 + i), q4[2 * i], q4[2 * i + 1], METRIC, a0, a1, a2, a3);
+    } else {
+        uint4 v[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) v[i] = __ldg(x4 + i);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) acc8(v[i], q4[2 * i], q4[2 * i + 1], METRIC, a0, a1, a2, a3);
+    }
+    const float s = (a0 + a1) + (a2 + a3);
+    return METRIC == 0 ? s : -s;
 }
 
 __device__ __forceinline__ uint64_t warp_min64(uint64_t v) {

@@ -136,8 +136,14 @@ void run_host_stages(const HostStageArgs& a) {
             for (int j = 0; j < a.ef1; ++j) {
                 const int32_t v = ci[j];
                 if (v < 0) continue;
-                float res = dr > 0 ? dist_full(qh.data() + dp, a.rotated + (int64_t)v * D + dp, dr, a.metric) : 0.f;
-                C.push_back(Cand{cd[j] + res, v, false});
+                float full;
+                if (a.recompute_primary) {
+                    full = dfull(v);
+                } else {
+                    const float res = dr > 0 ? dist_full(qh.data() + dp, a.rotated + (int64_t)v * D + dp, dr, a.metric) : 0.f;
+                    full = cd[j] + res;
+                }
+                C.push_back(Cand{full, v, false});
                 vis.insert(v);
                 ++my2;
             }

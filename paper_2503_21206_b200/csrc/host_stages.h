@@ -25,6 +25,7 @@ struct HostStageArgs {
     const float* qres = nullptr;        // [m][dim − rdim]
     int32_t* out_ids = nullptr;         // [m][k]
     float* out_d = nullptr;             // [m][k]
+    bool recompute_primary = false;     // full δ from X̂ over all D dims instead of δ' + residual
     int64_t* sum_n_dist2 = nullptr;
     int64_t* sum_n_dist3 = nullptr;
     // Optional pipelining hook: called before a worker first touches a query of a

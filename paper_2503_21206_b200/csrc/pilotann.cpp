@@ -18,6 +18,7 @@
 #include <unordered_set>
 #include <vector>
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "host_stages.h"
@@ -426,6 +427,23 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     for (int64_t i = 0; i < (int64_t)r * dp; ++i)
         if (!std::isfinite(p->fes_centroids[i])) return fail(PA_EINVAL, "non-finite centroid");
 
+    // NEXT-f1 storage: reduced rows rounded once to binary16 (RNE); every stage-①
+    // distance and the FES pool then use exactly these rounded values.
+    std::vector<float> red16;
+    const float* RED = p->reduced;
+    if (p->reduced_fp16) {
+        red16.resize((size_t)n * dp);
+        bool bad = false;
+        parallel_rows(n, [&](int64_t lo, int64_t hi) {
+            for (int64_t i = lo * dp; i < hi * dp; ++i) {
+                const float v = __half2float(__float2half_rn(p->reduced[i]));
+                red16[i] = v;
+                if (!std::isfinite(v) && member[i / dp]) bad = true;
+            }
+        });
+        if (bad) return fail(PA_EINVAL, "reduced value outside the binary16 range");
+        RED = red16.data();
+    }
     // ---- device replica
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
@@ -445,6 +463,9 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     d.max_cell = (int32_t)((max_cell + 3) & ~3);
     d.ell_w = p->max_degree <= 32 ? 32 : 64;
     const int dps = d.rdim_pad;
+    d.rdim_h = (dp + 7) & ~7;
+    d.qlen = p->reduced_fp16 ? std::max(dps, d.rdim_h) : dps;
+    const bool f16 = p->reduced_fp16 != 0;
     auto bail = [&](pa_status s) { pa_destroy(ix); return s; };
     {
         std::lock_guard<std::mutex> g(g_reg_mu);
@@ -462,31 +483,48 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     for (auto& e : ix->ev) CUB(cudaEventCreate(&e));
     CUB(dalloc(&d.basis, (size_t)D * D));
     CUB(cudaMemcpy(d.basis, p->basis, sizeof(float) * D * D, cudaMemcpyHostToDevice));
-    // reduced vectors [n][dps] (zero rows for non-members), staged in chunks
-    CUB(dalloc(&d.reduced, (size_t)n * dps));
+    // reduced vectors [n][dps] fp32 or [n][rdim_h] binary16 (zero rows for non-members), staged in chunks
+    if (f16) {
+        __half* rh = nullptr;
+        CUB(cudaMalloc((void**)&rh, sizeof(__half) * (size_t)n * d.rdim_h));
+        d.reduced_h = rh;
+    } else {
+        CUB(dalloc(&d.reduced, (size_t)n * dps));
+    }
     CUB(dalloc(&d.ell, (size_t)n * d.ell_w));
     {
         const int64_t chunk = 1 << 20;
         std::vector<float> rb((size_t)std::min(chunk, n) * dps);
+        std::vector<__half> hb(f16 ? (size_t)std::min(chunk, n) * d.rdim_h : 0);
         std::vector<int32_t> eb((size_t)std::min(chunk, n) * d.ell_w);
         for (int64_t s0 = 0; s0 < n; s0 += chunk) {
             int64_t s1 = std::min(n, s0 + chunk);
             parallel_rows(s1 - s0, [&](int64_t lo, int64_t hi) {
                 for (int64_t i = lo; i < hi; ++i) {
                     int64_t u = s0 + i;
-                    float* dst = &rb[(size_t)i * dps];
-                    if (member[u]) {
-                        std::memcpy(dst, p->reduced + u * dp, sizeof(float) * dp);
-                        for (int j = dp; j < dps; ++j) dst[j] = 0.f;
+                    if (f16) {
+                        __half* dh = &hb[(size_t)i * d.rdim_h];
+                        for (int j = 0; j < d.rdim_h; ++j)
+                            dh[j] = __float2half_rn(member[u] && j < dp ? RED[u * dp + j] : 0.f);
                     } else {
-                        std::memset(dst, 0, sizeof(float) * dps);
+                        float* dst = &rb[(size_t)i * dps];
+                        if (member[u]) {
+                            std::memcpy(dst, RED + u * dp, sizeof(float) * dp);
+                            for (int j = dp; j < dps; ++j) dst[j] = 0.f;
+                        } else {
+                            std::memset(dst, 0, sizeof(float) * dps);
+                        }
                     }
                     int32_t* row = &eb[(size_t)i * d.ell_w];
                     int64_t a0 = p->sub_offsets[u], a1 = p->sub_offsets[u + 1];
                     for (int j = 0; j < d.ell_w; ++j) row[j] = (a0 + j < a1) ? p->sub_neighbors[a0 + j] : -1;
                 }
             });
-            CUB(cudaMemcpy(d.reduced + s0 * dps, rb.data(), sizeof(float) * (s1 - s0) * dps, cudaMemcpyHostToDevice));
+            if (f16)
+                CUB(cudaMemcpy(static_cast<__half*>(d.reduced_h) + s0 * d.rdim_h, hb.data(),
+                               sizeof(__half) * (s1 - s0) * d.rdim_h, cudaMemcpyHostToDevice));
+            else
+                CUB(cudaMemcpy(d.reduced + s0 * dps, rb.data(), sizeof(float) * (s1 - s0) * dps, cudaMemcpyHostToDevice));
             CUB(cudaMemcpy(d.ell + s0 * d.ell_w, eb.data(), sizeof(int32_t) * (s1 - s0) * d.ell_w, cudaMemcpyHostToDevice));
         }
     }
@@ -504,13 +542,13 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
         CUB(cudaMemcpy(d.pool_ids, p->fes_pool_ids, sizeof(int32_t) * pool_n, cudaMemcpyHostToDevice));
         std::vector<float> pv((size_t)pool_n * dps, 0.f);
         for (int64_t j = 0; j < pool_n; ++j)
-            std::memcpy(&pv[(size_t)j * dps], p->reduced + (int64_t)p->fes_pool_ids[j] * dp, sizeof(float) * dp);
+            std::memcpy(&pv[(size_t)j * dps], RED + (int64_t)p->fes_pool_ids[j] * dp, sizeof(float) * dp);
         CUB(dalloc(&d.pool_vec, pv.size()));
         CUB(cudaMemcpy(d.pool_vec, pv.data(), sizeof(float) * pv.size(), cudaMemcpyHostToDevice));
         std::vector<float> pn((size_t)pool_n);
         for (int64_t j = 0; j < pool_n; ++j) {
             double s2 = 0;
-            const float* e = p->reduced + (int64_t)p->fes_pool_ids[j] * dp;
+            const float* e = RED + (int64_t)p->fes_pool_ids[j] * dp;
             for (int i = 0; i < dp; ++i) s2 += (double)e[i] * e[i];
             pn[j] = (float)s2;
         }
@@ -531,7 +569,7 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
             const int64_t b = p->fes_cell_off[c], nc = p->fes_cell_off[c + 1] - b;
             for (int64_t e = 0; e < nc; ++e) {
                 const int ch = choff[c] + (int)(e / 128), row = (int)(e % 128);
-                const float* src = p->reduced + (int64_t)p->fes_pool_ids[b + e] * dp;
+                const float* src = RED + (int64_t)p->fes_pool_ids[b + e] * dp;
                 for (int kc = 0; kc < kch; ++kc) {
                     float* hi = &img[(((size_t)ch * kch + kc) * 2 + 0) * 4096];
                     float* lo = &img[(((size_t)ch * kch + kc) * 2 + 1) * 4096];
@@ -702,6 +740,7 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
         h.flags = r.flags; h.threads = r.threads;
         h.cand_ids = ix->h_cand_ids; h.cand_d = ix->h_cand_d; h.qp = ix->h_qp; h.qp_stride = d.rdim_pad;
         h.qres = ix->h_qres; h.out_ids = out_ids; h.out_d = out_d;
+        h.recompute_primary = d.reduced_h != nullptr;   // δ' was computed on rounded rows
         int64_t s2 = 0, s3 = 0;
         h.sum_n_dist2 = &s2; h.sum_n_dist3 = &s3;
         h.ready_ctx = &ready;
@@ -796,7 +835,7 @@ void pa_destroy(pa_index* ix) {
     cudaFreeHost(ix->h_cand_ids); cudaFreeHost(ix->h_cand_d); cudaFreeHost(ix->h_qp); cudaFreeHost(ix->h_qres);
     cudaFreeHost(ix->h_counters);
     auto& d = ix->dev;
-    cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
+    cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.reduced_h); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
     cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
     cudaFree(d.pool_img); cudaFree(d.chunk_off);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);

@@ -7,10 +7,14 @@
 
 namespace pa {
 namespace trav {
-void* traverse_pick_0c(int ef, int dps, bool trace);
-void* traverse_pick_0w(int ef, int dps, bool trace);
-void* traverse_pick_1c(int ef, int dps, bool trace);
-void* traverse_pick_1w(int ef, int dps, bool trace);
+void* traverse_pick_0cf(int ef, int d, bool trace);
+void* traverse_pick_0wf(int ef, int d, bool trace);
+void* traverse_pick_1cf(int ef, int d, bool trace);
+void* traverse_pick_1wf(int ef, int d, bool trace);
+void* traverse_pick_0ch(int ef, int d, bool trace);
+void* traverse_pick_0wh(int ef, int d, bool trace);
+void* traverse_pick_1ch(int ef, int d, bool trace);
+void* traverse_pick_1wh(int ef, int d, bool trace);
 constexpr int kTW = 4;
 }  // namespace trav
 
@@ -24,13 +28,19 @@ bool use_compact(const DevIndex& ix, const SearchArgs& a) {
 }
 void* pick(const DevIndex& ix, const SearchArgs& a) {
     const bool cp = use_compact(ix, a), tr = a.trace_cap > 0;
-    if (ix.metric == 0) return cp ? trav::traverse_pick_0c(a.ef, ix.rdim_pad, tr) : trav::traverse_pick_0w(a.ef, ix.rdim_pad, tr);
-    return cp ? trav::traverse_pick_1c(a.ef, ix.rdim_pad, tr) : trav::traverse_pick_1w(a.ef, ix.rdim_pad, tr);
+    if (ix.reduced_h) {
+        const int d = ix.rdim_h;
+        if (ix.metric == 0) return cp ? trav::traverse_pick_0ch(a.ef, d, tr) : trav::traverse_pick_0wh(a.ef, d, tr);
+        return cp ? trav::traverse_pick_1ch(a.ef, d, tr) : trav::traverse_pick_1wh(a.ef, d, tr);
+    }
+    const int d = ix.rdim_pad;
+    if (ix.metric == 0) return cp ? trav::traverse_pick_0cf(a.ef, d, tr) : trav::traverse_pick_0wf(a.ef, d, tr);
+    return cp ? trav::traverse_pick_1cf(a.ef, d, tr) : trav::traverse_pick_1wf(a.ef, d, tr);
 }
 
 size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
     const size_t efp = (size_t)((a.ef + 1) & ~1);
-    size_t per_warp = efp * 8 + (size_t)ix.rdim_pad * 4 + ((size_t)(use_compact(ix, a) ? 2 : 4) << a.hash_log2);
+    size_t per_warp = efp * 8 + (size_t)ix.qlen * 4 + ((size_t)(use_compact(ix, a) ? 2 : 4) << a.hash_log2);
     return per_warp * kTW;
 }
 }  // namespace

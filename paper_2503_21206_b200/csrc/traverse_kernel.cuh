@@ -137,18 +137,19 @@ __device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
     return false;
 }
 
-template <int METRIC, bool COMPACT, int SMAX, int DPS4, bool TRACE>
+template <int METRIC, bool COMPACT, int SMAX, int DPS4, bool TRACE, bool H16>
 __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix, SearchArgs a) {
     const int ELLW = ix.ell_w, NCH = ix.ell_w >> 5;         // ELL row width 32 or 64
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
     const int efp = (ef + 1) & ~1;                      // keep qs 16-B aligned
-    const size_t per_warp = (size_t)efp * 8 + (size_t)dps * 4 + (size_t)S * (COMPACT ? 2 : 4);
+    const int qlen = ix.qlen;                           // ≥ dps (fp32 rows) / ≥ rdim_h (fp16 rows)
+    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 + (size_t)S * (COMPACT ? 2 : 4);
     unsigned char* base = smem_raw + per_warp * w;
     uint64_t* C = reinterpret_cast<uint64_t*>(base);
     float* qs = reinterpret_cast<float*>(C + efp);
-    int32_t* H = reinterpret_cast<int32_t*>(qs + dps);
+    int32_t* H = reinterpret_cast<int32_t*>(qs + qlen);
     const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t gw = (int64_t)blockIdx.x * kTW + w;
 
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
         if (q >= a.m) break;
         vs.count1 = 0;
         vs.count2 = 0;
-        for (int i = lane; i < dps; i += 32) qs[i] = a.qp[q * dps + i];
+        for (int i = lane; i < qlen; i += 32) qs[i] = i < dps ? a.qp[q * dps + i] : 0.f;
         int4* H4 = reinterpret_cast<int4*>(H);
         for (int i = lane; i < (S >> (COMPACT ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
         __syncwarp();
@@ -201,7 +202,15 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
         auto merge_batch = [&](int32_t v, bool isnew, auto&& before_merge) {
             if (__ballot_sync(kFull, isnew) == 0) { before_merge(); return; }
             uint64_t key = kKeyInf;
-            if (isnew) key = make_key(row_dist_t<METRIC, DPS4>(qs, ix.reduced + (int64_t)v * dps, dps), v);
+            if (isnew) {
+                float dv;
+                if constexpr (H16)
+                    dv = row_dist_h<METRIC, DPS4>(qs, reinterpret_cast<const __half*>(ix.reduced_h) + (int64_t)v * ix.rdim_h,
+                                                  ix.rdim_h);
+                else
+                    dv = row_dist_t<METRIC, DPS4>(qs, ix.reduced + (int64_t)v * dps, dps);
+                key = make_key(dv, v);
+            }
             {
                 const uint32_t hi = __reduce_min_sync(kFull, (uint32_t)(key >> 32));
                 const uint32_t lo = __reduce_min_sync(kFull, (uint32_t)(key >> 32) == hi ? (uint32_t)key : 0xffffffffu);
@@ -283,7 +292,10 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
                         for (int c2 = 0; c2 < 2; ++c2) {
                             const int32_t w2 = sv[c2];
                             if (w2 >= 0 && !visited_l1<COMPACT>(vs, w2))
-                                prefetch_row_l2(ix.reduced + (int64_t)w2 * dps, dps * 4);
+                                prefetch_row_l2(H16 ? (const void*)(reinterpret_cast<const __half*>(ix.reduced_h) +
+                                                                     (int64_t)w2 * ix.rdim_h)
+                                                    : (const void*)(ix.reduced + (int64_t)w2 * dps),
+                                                H16 ? ix.rdim_h * 2 : dps * 4);
                         }
                     }
                     if (status == 0)

@@ -222,3 +222,47 @@ def test_full_pipeline_parity(cfg_name, request):
     want = ((X - Qh[:, None, :]) ** 2).sum(2) if cfg.metric == "l2" else -(X * Qh[:, None, :]).sum(2)
     scale = np.abs(want) if cfg.metric == "l2" else np.abs(X * Qh[:, None, :]).sum(2)
     assert np.all(np.abs(d - want) <= 1e-5 * scale + 1e-6 * np.sqrt(np.abs(want) * (Qh ** 2).sum(1, keepdims=True)))
+
+
+# ---------------------------------------------------------------- NEXT-f1 ---
+def rounded16(inst):
+    """The oracle side of binary16 storage: the identical rounded values (RNE)."""
+    return dict(inst, reduced=inst["reduced"].astype(np.float16).astype(np.float32))
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_fp16_storage_integer_fixture_bit_exact(metric):
+    inst = integer_instance(seed=4, metric=metric)
+    ix = pa.Index.from_instance(inst, reduced_fp16=True)
+    g = run_gpu(ix, inst, 5, 32, trace_cap=4096)
+    ix.close()
+    r = orc.search(rounded16(inst), k=5, ef=32, stages=1, trace_cap=4096)
+    rep = compare(rounded16(inst), g, r, 5, 32)
+    assert not rep.fail and rep.tie == 0, (rep, rep.fail[:3])
+    assert np.array_equal(g["ids"], r["ids"]) and np.array_equal(g["d"].astype(np.float64), r["d"])
+
+
+@pytest.mark.parametrize("cfg_name", ["S1", "S2"])
+def test_fp16_storage_parity(cfg_name, request):
+    inst = request.getfixturevalue(cfg_name.lower())
+    cfg = inst["cfg"]
+    ix = pa.Index.from_instance(inst, reduced_fp16=True)
+    g = run_gpu(ix, inst, cfg.k, cfg.ef, trace_cap=8192)
+    ix.close()
+    inst16 = rounded16(inst)
+    r = orc.search(inst16, k=cfg.k, ef=cfg.ef, stages=1, trace_cap=8192)
+    rep = compare(inst16, g, r, cfg.k, cfg.ef, gt_ids=inst["gt_sub_ids"][:, :cfg.k])
+    print(cfg_name, "fp16", rep, rep.recall_gpu, rep.recall_orc)
+    assert not rep.fail, rep.fail[:5]
+    assert rep.exact >= 0.9 * cfg.m
+
+
+def test_fp16_storage_full_pipeline(s1):
+    cfg = s1["cfg"]
+    ix = pa.Index.from_instance(s1, reduced_fp16=True)
+    ix.attach_host(s1["full_offsets"], s1["full_neighbors"], s1["rotated"])
+    ids, d = ix.search(s1["queries"], k=cfg.k, ef=cfg.ef, stages=pa.PA_STAGES_FULL)
+    ix.close()
+    r = orc.search(rounded16(s1), k=cfg.k, ef=cfg.ef, stages=3)
+    gt = s1["gt_ids"][:, :cfg.k]
+    assert abs(orc.recall(ids, gt, cfg.k) - orc.recall(r["ids"], gt, cfg.k)) <= 0.002 + 1e-12
