@@ -399,6 +399,118 @@ __global__ void __launch_bounds__(128) k_fes_select(FesParams p, int64_t m) {
     }
 }
 
+// Selection, two passes (far fewer instructions than merging every passing key):
+//   1. every lane keeps the KP = ceil(E/32) smallest keys of its strided share in
+//      registers; a bitwise search over the high (distance) words of those 32·KP
+//      candidates gives T = the distance word of their E-th smallest — a bound ≥
+//      the true E-th smallest distance of the row;
+//   2. all keys with distance word ≤ T (the true top-E and typically a few more)
+//      are compacted into a per-warp smem buffer and bitonic-sorted once; the
+//      first E are the entries.  A row with more than kSelCap candidates (heavy
+//      ties) falls back to the threshold + rank-merge loop.
+constexpr int kSelCap = 512;
+
+__device__ __forceinline__ void warp_bitonic_smem(uint64_t* a, int n, int lane) {
+    for (int k = 2; k <= n; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < n; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t x = a[i], y = a[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) { a[i] = y; a[ixj] = x; }
+                }
+            }
+            __syncwarp();
+        }
+}
+
+template <int KPMAX, int SMAX>
+__global__ void __launch_bounds__(128) k_fes_select2(FesParams p, int64_t m) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int E = p.E, KP = (E + 31) / 32;
+    uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)w * kSelCap;
+    const int64_t nwarps = (int64_t)gridDim.x * 4;
+    for (int64_t pos = (int64_t)blockIdx.x * 4 + w; pos < m; pos += nwarps) {
+        int c = 0;
+        while (c + 1 < p.r && p.qoff[c + 1] <= pos) ++c;
+        const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
+        const float* srow = p.scores + pos * p.sstride;
+        const int32_t* prow = p.pool_ids + pb;
+        const int32_t q = p.perm[pos];
+        // ---- pass 1: per-lane KP smallest keys
+        uint64_t t[KPMAX];
+#pragma unroll
+        for (int i = 0; i < KPMAX; ++i) t[i] = kKeyInf;
+        for (int j = lane; j < nc; j += 32) {
+            const uint64_t key = make_key(srow[j], __ldg(prow + j));
+            if (key < t[KP - 1]) {
+                uint64_t x = key;
+#pragma unroll
+                for (int i = 0; i < KPMAX; ++i) {
+                    if (i < KP && x < t[i]) { const uint64_t y = t[i]; t[i] = x; x = y; }
+                }
+            }
+        }
+        // bitwise search for T = high word of the E-th smallest candidate
+        uint32_t T = 0xffffffffu;
+        if (nc > E) {
+            uint32_t lo = 0;                           // build T bit by bit: largest T with count(< T) < E
+            for (int b = 31; b >= 0; --b) {
+                const uint32_t trial = lo | (1u << b);
+                int cnt = 0;
+#pragma unroll
+                for (int i = 0; i < KPMAX; ++i) cnt += (i < KP && (uint32_t)(t[i] >> 32) < trial) ? 1 : 0;
+                cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
+                if (cnt < E) lo = trial;
+            }
+            T = lo;                                    // count(word < T) < E ≤ count(word ≤ T)
+        }
+        // ---- pass 2: compact all keys with distance word ≤ T, sort once
+        int M = 0;
+        bool overflow = false;
+        for (int j0 = 0; j0 < nc && !overflow; j0 += 32) {
+            const int j = j0 + lane;
+            uint64_t key = kKeyInf;
+            bool in = false;
+            if (j < nc) {
+                key = make_key(srow[j], __ldg(prow + j));
+                in = (uint32_t)(key >> 32) <= T;
+            }
+            const unsigned bal = __ballot_sync(kFull, in);
+            const int add = __popc(bal);
+            if (M + add > kSelCap) { overflow = true; break; }
+            if (in) buf[M + __popc(bal & ((1u << lane) - 1u))] = key;
+            M += add;
+        }
+        __syncwarp();
+        if (!overflow) {
+            int n2 = 32;
+            while (n2 < M) n2 <<= 1;
+            for (int i = M + lane; i < n2; i += 32) buf[i] = kKeyInf;
+            __syncwarp();
+            warp_bitonic_smem(buf, n2, lane);
+            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < M ? key_id(buf[j]) : -1;
+        } else {                                       // heavy ties: merge path
+            uint64_t* C = buf;
+            int csz = 0;
+            for (int j0 = 0; j0 < nc; j0 += 32) {
+                const int j = j0 + lane;
+                const uint64_t key = j < nc ? make_key(srow[j], __ldg(prow + j)) : kKeyInf;
+                const uint64_t thresh = csz == E ? C[E - 1] : kKeyInf;
+                const bool pass = key < thresh;
+                const unsigned pbal = __ballot_sync(kFull, pass);
+                if (pbal == 0) continue;
+                int minr;
+                csz = rank_merge<SMAX>(C, csz, E, key, pass, pbal, lane, minr);
+            }
+            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < csz ? key_id(C[j]) : -1;
+        }
+        __syncwarp();
+    }
+}
+
 size_t fes_scores_smem(int kch) { return (size_t)kch * 2 * 16384 + 2 * 16384 + 16; }
 
 }  // namespace
@@ -435,8 +547,17 @@ int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
     }
-    void* sel = a.E <= 64 ? (void*)k_fes_select<2> : a.E <= 128 ? (void*)k_fes_select<4> : (void*)k_fes_select<8>;
-    const size_t ssm = (size_t)4 * a.E * 8;
+    const char* se = std::getenv("PA_FES_SELECT");
+    void* sel;
+    size_t ssm;
+    if (se && !std::strcmp(se, "merge")) {
+        sel = a.E <= 64 ? (void*)k_fes_select<2> : a.E <= 128 ? (void*)k_fes_select<4> : (void*)k_fes_select<8>;
+        ssm = (size_t)4 * a.E * 8;
+    } else {
+        sel = a.E <= 64 ? (void*)k_fes_select2<2, 2> : a.E <= 96 ? (void*)k_fes_select2<3, 4>
+            : a.E <= 128 ? (void*)k_fes_select2<4, 4> : (void*)k_fes_select2<8, 8>;
+        ssm = (size_t)4 * kSelCap * 8;
+    }
     cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     int64_t blocks = (a.m + 3) / 4;
     int64_t m = a.m;

@@ -266,3 +266,20 @@ def test_fp16_storage_full_pipeline(s1):
     r = orc.search(rounded16(s1), k=cfg.k, ef=cfg.ef, stages=3)
     gt = s1["gt_ids"][:, :cfg.k]
     assert abs(orc.recall(ids, gt, cfg.k) - orc.recall(r["ids"], gt, cfg.k)) <= 0.002 + 1e-12
+
+
+@pytest.mark.parametrize("cfg_name", ["S1", "S2", "C0"])
+def test_fes_selection_variants_agree(cfg_name, request, monkeypatch):
+    """The two-pass (threshold + single sort) FES selection returns exactly the
+    entries of the rank-merge selection (same GEMM scores, same keys)."""
+    inst = request.getfixturevalue(cfg_name.lower())
+    cfg = inst["cfg"]
+    ix = pa.Index.from_instance(inst)
+    outs = []
+    for sel in ("two-pass", "merge"):
+        monkeypatch.setenv("PA_FES_SELECT", sel)
+        for ef in (10, 64, 96, 256):
+            outs.append(run_gpu(ix, inst, cfg.k, ef)["entries"])
+    ix.close()
+    for a, b in zip(outs[:4], outs[4:]):
+        assert np.array_equal(a, b)
