@@ -257,41 +257,79 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- timed region: W warm-up, K steps; L2 flushed between steps (512 MB write)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    for _ in range(args.warmup):
-        step(ef)
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    trav_ms, proj_ms, fes_ms, launches, bytes_alg = [], [], [], 0, 0.0
     ell_w = 32 if int(np.diff(inst["sub_offsets"]).max()) <= 32 else 64
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+
+    def timed(step_fn, ixv, ef_, fp16, clk=None):
+        for _ in range(args.warmup):
+            step_fn(ef_)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        acc = dict(trav=[], proj=[], fes=[], launches=0, bytes=0.0)
+        row_bytes = 2 * ((cfg.dp + 7) // 8 * 8) if fp16 else 4 * cfg.dp
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         for i in range(args.steps):
             flush.fill_(float(i))
             ev[i][0].record(stream)
-            step(ef)
+            step_fn(ef_)
             ev[i][1].record(stream)
-            st = ix.stats()                       # syncs the traversal events of this step
-            trav_ms.append(st["ms_traverse"])
-            proj_ms.append(st["ms_project"])
-            fes_ms.append(st["ms_fes"])
-            launches += st["kernel_launches"]
-            row_bytes = 2 * ((cfg.dp + 7) // 8 * 8) if args.reduced == "fp16" else 4 * cfg.dp
-            bytes_alg = st["sum_n_exp"] * 4 * ell_w + st["sum_n_dist"] * row_bytes
+            st = ixv.stats()                      # syncs the traversal events of this step (outside the events)
+            acc["trav"].append(st["ms_traverse"])
+            acc["proj"].append(st["ms_project"])
+            acc["fes"].append(st["ms_fes"])
+            acc["launches"] += st["kernel_launches"]
+            acc["bytes"] = st["sum_n_exp"] * 4 * ell_w + st["sum_n_dist"] * row_bytes
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    ms = sum(step_ms) / len(step_ms)
-    trav = sum(trav_ms) / len(trav_ms)
+        if world > 1:
+            dist.barrier()
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        ms_, trav_ = sum(step_ms) / len(step_ms), sum(acc["trav"]) / len(acc["trav"])
+        if world > 1:
+            t = torch.tensor([ms_, trav_], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_, trav_ = float(t[0]), float(t[1])
+        acc.update(ms=ms_, trav_ms=trav_)
+        return acc
+
+    with ClockSampler(local_rank) as clk:
+        main = timed(step, ix, ef, args.reduced == "fp16")
+    ms, trav, launches, bytes_alg = main["ms"], main["trav_ms"], main["launches"], main["bytes"]
+    trav_ms, proj_ms, fes_ms = main["trav"], main["proj"], main["fes"]
     rec = recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k)
     rec_full = recall_at(out_i.cpu().numpy(), inst["gt_ids"], k)
-    if world > 1:
-        t = torch.tensor([ms, trav], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, trav = float(t[0]), float(t[1])
     qps = m * world / (ms / 1e3)
+
+    # ---- NEXT-f1 variant: the same search with binary16-stored reduced rows
+    f1 = None
+    if args.reduced == "fp32" and not args.no_f1:
+        ix16 = pa.Index.from_instance(inst, device=local_rank, reduced_fp16=True)
+
+        def step16(e):
+            ix16.search_device(qd, k, e, out_i, out_d, stream=stream.cuda_stream)
+        ef16 = None
+        for e in EF_SWEEP:
+            step16(e)
+            torch.cuda.synchronize()
+            if recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k) >= TARGET_RECALL:
+                ef16 = e
+                break
+        ef16 = ef16 or EF_SWEEP[-1]
+        if world > 1:
+            t = torch.tensor([ef16], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ef16 = int(t.item())
+        v = timed(step16, ix16, ef16, True)
+        r16 = recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k)
+        pk, _ = measured_peaks()
+        ach = v["bytes"] / (v["trav_ms"] / 1e3) / 1e9
+        f1 = {"what": "NEXT-f1: reduced rows stored as binary16 (rounded once at build; fp32 arithmetic; "
+                      "parity vs the oracle on the same rounded values)",
+              "value": round(m * world / (v["ms"] / 1e3), 1), "unit": "queries/s", "ef": ef16,
+              "recall_at_10_gt_sub": round(r16, 4), "ms_per_step": round(v["ms"], 4),
+              "traverse_ms": round(v["trav_ms"], 4), "alg_bytes_per_launch": v["bytes"],
+              "roofline_frac": round(ach / pk, 4), "achieved_gbs": round(ach, 1)}
+        ix16.close()
 
     # ---- e2e through the public host API: pinned host queries in, host results out
     hq = torch.from_numpy(inst["queries"]).pin_memory()
@@ -347,6 +385,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": m * cfg.D * 4,
                     "d2h_bytes_per_step": m * k * 8},
             "end_to_end_full": full,
+            "f1_fp16_storage": f1,
             "gpu_launches": launches,
             "clocks": clocks,
         }
@@ -413,6 +452,7 @@ def main():
     ap.add_argument("--full-sweep", action="store_true")
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-f1", action="store_true", help="skip the binary16-storage (NEXT-f1) variant")
     ap.add_argument("--cache", default=None, help="dir to cache the generated instance (same-call reuse only)")
     ap.add_argument("--repeat-queries", type=int, default=1, help="experiment only: tile the query batch R times")
     ap.add_argument("--reduced", default="fp32", choices=["fp32", "fp16"],

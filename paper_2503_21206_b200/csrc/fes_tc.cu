@@ -443,13 +443,25 @@ __global__ void __launch_bounds__(128) k_fes_select2(FesParams p, int64_t m) {
         uint64_t t[KPMAX];
 #pragma unroll
         for (int i = 0; i < KPMAX; ++i) t[i] = kKeyInf;
-        for (int j = lane; j < nc; j += 32) {
-            const uint64_t key = make_key(srow[j], __ldg(prow + j));
-            if (key < t[KP - 1]) {
-                uint64_t x = key;
+        for (int j0 = 0; j0 < nc; j0 += 128) {              // 4 loads in flight per lane
+            float sv[4];
+            int32_t iv[4];
 #pragma unroll
-                for (int i = 0; i < KPMAX; ++i) {
-                    if (i < KP && x < t[i]) { const uint64_t y = t[i]; t[i] = x; x = y; }
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + u * 32 + lane;
+                sv[u] = j < nc ? srow[j] : 0.f;
+                iv[u] = j < nc ? __ldg(prow + j) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (j0 + u * 32 + lane >= nc) continue;
+                const uint64_t key = make_key(sv[u], iv[u]);
+                if (key < t[KP - 1]) {
+                    uint64_t x = key;
+#pragma unroll
+                    for (int i = 0; i < KPMAX; ++i) {
+                        if (i < KP && x < t[i]) { const uint64_t y = t[i]; t[i] = x; x = y; }
+                    }
                 }
             }
         }
