@@ -15,6 +15,15 @@ void* traverse_pick_0ch(int ef, int d, bool trace);
 void* traverse_pick_0wh(int ef, int d, bool trace);
 void* traverse_pick_1ch(int ef, int d, bool trace);
 void* traverse_pick_1wh(int ef, int d, bool trace);
+void* traverse_pick_pipe_0cf(int ef, int d, bool trace);
+void* traverse_pick_pipe_0ch(int ef, int d, bool trace);
+void* traverse_pick_pipe_0wf(int ef, int d, bool trace);
+void* traverse_pick_pipe_0wh(int ef, int d, bool trace);
+void* traverse_pick_pipe_1cf(int ef, int d, bool trace);
+void* traverse_pick_pipe_1ch(int ef, int d, bool trace);
+void* traverse_pick_pipe_1wf(int ef, int d, bool trace);
+void* traverse_pick_pipe_1wh(int ef, int d, bool trace);
+
 constexpr int kTW = 4;
 }  // namespace trav
 
@@ -28,6 +37,17 @@ bool use_compact(const DevIndex& ix, const SearchArgs& a) {
 }
 void* pick(const DevIndex& ix, const SearchArgs& a) {
     const bool cp = use_compact(ix, a), tr = a.trace_cap > 0;
+    const char* ve = std::getenv("PA_TRAVERSE");
+    if (ix.ell_w == 32 && !(ve && !std::strcmp(ve, "v1"))) {        // software-pipelined kernel
+        const bool h = ix.reduced_h != nullptr;
+        const int d = h ? ix.rdim_h : ix.rdim_pad;
+        if (ix.metric == 0) {
+            if (cp) return h ? trav::traverse_pick_pipe_0ch(a.ef, d, tr) : trav::traverse_pick_pipe_0cf(a.ef, d, tr);
+            return h ? trav::traverse_pick_pipe_0wh(a.ef, d, tr) : trav::traverse_pick_pipe_0wf(a.ef, d, tr);
+        }
+        if (cp) return h ? trav::traverse_pick_pipe_1ch(a.ef, d, tr) : trav::traverse_pick_pipe_1cf(a.ef, d, tr);
+        return h ? trav::traverse_pick_pipe_1wh(a.ef, d, tr) : trav::traverse_pick_pipe_1wf(a.ef, d, tr);
+    }
     if (ix.reduced_h) {
         const int d = ix.rdim_h;
         if (ix.metric == 0) return cp ? trav::traverse_pick_0ch(a.ef, d, tr) : trav::traverse_pick_0wh(a.ef, d, tr);

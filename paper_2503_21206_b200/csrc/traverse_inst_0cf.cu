@@ -16,6 +16,17 @@ void* pick4(int d, bool trace) {
         default: return (void*)k_traverse<METRIC, COMPACT, SMAX, 0, false, false>;
     }
 }
+template <int METRIC, bool COMPACT, int SMAX>
+void* pick4p(int d, bool trace) {
+    if (trace) return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 0, true, false>;
+    switch (d) {
+        case 32: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 8, false, false>;
+        case 48: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 12, false, false>;
+        case 64: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 16, false, false>;
+        case 128: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 32, false, false>;
+        default: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 0, false, false>;
+    }
+}
 }  // namespace
 
 void* traverse_pick_0cf(int ef, int d, bool trace) {
@@ -25,6 +36,14 @@ void* traverse_pick_0cf(int ef, int d, bool trace) {
     if (ef <= 96) return pick4<METRIC, COMPACT, 3>(d, trace);
     if (ef <= 128) return pick4<METRIC, COMPACT, 4>(d, trace);
     return pick4<METRIC, COMPACT, 8>(d, trace);
+}
+void* traverse_pick_pipe_0cf(int ef, int d, bool trace) {
+    constexpr int METRIC = 0;
+    constexpr bool COMPACT = true;
+    if (ef <= 64) return pick4p<METRIC, COMPACT, 2>(d, trace);
+    if (ef <= 96) return pick4p<METRIC, COMPACT, 3>(d, trace);
+    if (ef <= 128) return pick4p<METRIC, COMPACT, 4>(d, trace);
+    return pick4p<METRIC, COMPACT, 8>(d, trace);
 }
 }  // namespace trav
 }  // namespace pa

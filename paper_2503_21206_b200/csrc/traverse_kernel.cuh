@@ -341,5 +341,199 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Software-pipelined variant (ELL width 32).  Same algorithm, reordered so the
+// gather latency of expansion i overlaps the merge of expansion i−1's keys:
+//   1. visit u_i's neighbours; L2 bulk-prefetch the rows of the new ones;
+//   2. merge the passing keys of expansion i−1 into C; scan C for its best
+//      unchecked key r (the runner-up) and load r's ELL row speculatively;
+//   3. δ' of u_i's new neighbours (rows now in L2), filter against C's worst;
+//   4. u_{i+1} = min(r, best passing new key) — exactly Alg 1's next "first
+//      unchecked node": r is C's best unchecked, and a passing new key beats C's
+//      worst, so both are in the ef-truncated list; it is marked checked (in C,
+//      or on the pending key before it is merged) and its row is fetched.
+// The expansion and visit sequences are identical to the sequential kernel.
+template <int METRIC, bool COMPACT, int SMAX, int DPS4, bool TRACE, bool H16>
+__global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevIndex ix, SearchArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
+    const int efp = (ef + 1) & ~1;
+    const int qlen = ix.qlen;
+    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 + (size_t)S * (COMPACT ? 2 : 4);
+    unsigned char* base = smem_raw + per_warp * w;
+    uint64_t* C = reinterpret_cast<uint64_t*>(base);
+    float* qs = reinterpret_cast<float*>(C + efp);
+    int32_t* H = reinterpret_cast<int32_t*>(qs + qlen);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int64_t gw = (int64_t)blockIdx.x * kTW + w;
+
+    Visited vs;
+    vs.H = H;
+    vs.log2S = a.hash_log2;
+    vs.G = reinterpret_cast<uint32_t*>(a.spill + ((int64_t)gw << a.spill_log2));
+    vs.log = vs.G + ((size_t)1 << a.spill_log2);
+    vs.gmask = (1u << a.spill_log2) - 1u;
+    const int cap1 = S >> 1, cap2 = (int)(vs.gmask >> 1);
+
+    auto row_ptr = [&](int32_t v) -> const void* {
+        if constexpr (H16) return reinterpret_cast<const __half*>(ix.reduced_h) + (int64_t)v * ix.rdim_h;
+        else return ix.reduced + (int64_t)v * dps;
+    };
+    auto dist = [&](int32_t v) -> float {
+        if constexpr (H16) return row_dist_h<METRIC, DPS4>(qs, reinterpret_cast<const __half*>(row_ptr(v)), ix.rdim_h);
+        else return row_dist_t<METRIC, DPS4>(qs, reinterpret_cast<const float*>(row_ptr(v)), dps);
+    };
+    const int row_bytes = H16 ? ix.rdim_h * 2 : dps * 4;
+
+    for (;;) {
+        int64_t q = 0;
+        if (lane == 0) q = atomicAdd(a.work, 1);
+        q = __shfl_sync(kFull, (int)q, 0);
+        if (q >= a.m) break;
+        vs.count1 = 0;
+        vs.count2 = 0;
+        for (int i = lane; i < qlen; i += 32) qs[i] = i < dps ? a.qp[q * dps + i] : 0.f;
+        int4* H4 = reinterpret_cast<int4*>(H);
+        for (int i = lane; i < (S >> (COMPACT ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
+        __syncwarp();
+
+        int csz = 0, hint = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
+
+        auto visit_batch = [&](int32_t v) -> bool {
+            const bool open1 = vs.count1 + 32 <= cap1;
+            if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
+            bool l2 = false;
+            uint32_t slot = 0;
+            const bool isnew = v >= 0 && visit<COMPACT>(vs, v, open1, l2, slot);
+            const unsigned bal = __ballot_sync(kFull, isnew);
+            const unsigned bl2 = __ballot_sync(kFull, l2);
+            const int nnew = __popc(bal);
+            if (l2) vs.log[vs.count2 + __popc(bl2 & lt_mask)] = slot;
+            vs.count1 += nnew - __popc(bl2);
+            vs.count2 += __popc(bl2);
+            n_spill += __popc(bl2);
+            if (TRACE && isnew) {
+                const int pos = n_dist + __popc(bal & lt_mask);
+                if (pos < a.trace_cap) a.trace_visit[q * a.trace_cap + pos] = v;
+            }
+            n_dist += nnew;
+            return isnew;
+        };
+        auto merge_keys = [&](uint64_t key, bool pass, unsigned pb) {
+            if (pb == 0) return;
+            int minr;
+            csz = rank_merge<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
+            hint = min(hint, minr);
+        };
+        // ---- a5: C := entries, visited := entries (sequential merges)
+        for (int j0 = 0; j0 < a.E && status == 0; j0 += 32) {
+            const int j = j0 + lane;
+            const int32_t v = j < a.E ? a.entries[q * a.E + j] : -1;
+            const bool isnew = visit_batch(v);
+            if (status != 0) break;
+            const uint64_t key = isnew ? make_key(dist(v), v) : kKeyInf;
+            const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
+            const bool pass = key < thresh;
+            merge_keys(key, pass, __ballot_sync(kFull, pass));
+        }
+        // ---- a6: pipelined Alg 1 loop
+        if (!(a.flags & 4u) && status == 0) {
+            int p = -1;
+            for (int t = hint >> 5; t * 32 < csz; ++t) {
+                const int i = t * 32 + lane;
+                const unsigned b = __ballot_sync(kFull, i < csz && !key_checked(C[i]));
+                if (b) { p = t * 32 + __ffs(b) - 1; break; }
+            }
+            if (p >= 0) {
+                int32_t u = key_id(C[p]);
+                __syncwarp();
+                if (lane == 0) C[p] |= 1ull;
+                hint = p + 1;
+                int32_t vv = __ldg(ix.ell + (int64_t)u * 32 + lane);
+                uint64_t pkey = kKeyInf;          // pending keys of the previous expansion (unmerged)
+                bool ppass = false;
+                unsigned ppb = 0;
+                int32_t spec_u = -1, sv = -1;
+                for (int it = 0;; ++it) {
+                    if (TRACE && lane == 0 && n_exp < a.trace_cap) a.trace_expand[q * a.trace_cap + n_exp] = u;
+                    ++n_exp;
+                    // 1. visit u's neighbours, prefetch the new rows into L2
+                    const bool isnew = visit_batch(vv);
+                    if (status != 0) break;
+                    if (isnew) prefetch_row_l2(row_ptr(vv), row_bytes);
+                    // 2. merge the previous expansion's keys; runner-up r; its row speculatively
+                    merge_keys(pkey, ppass, ppb);
+                    ppb = 0;
+                    int pr = -1;
+                    for (int t = hint >> 5; t * 32 < csz; ++t) {
+                        const int i = t * 32 + lane;
+                        const unsigned b = __ballot_sync(kFull, i < csz && !key_checked(C[i]));
+                        if (b) { pr = t * 32 + __ffs(b) - 1; break; }
+                    }
+                    const uint64_t key_r = pr >= 0 ? C[pr] : kKeyInf;
+                    if (pr >= 0 && key_id(key_r) != spec_u) {
+                        spec_u = key_id(key_r);
+                        sv = __ldg(ix.ell + (int64_t)spec_u * 32 + lane);
+                    }
+                    // 3. δ' of the new neighbours, filter against C's worst
+                    const uint64_t key = isnew ? make_key(dist(vv), vv) : kKeyInf;
+                    const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
+                    bool pass = key < thresh;
+                    const unsigned pb = __ballot_sync(kFull, pass);
+                    uint64_t nstar = kKeyInf;
+                    if (pb) {
+                        const uint64_t kk = pass ? key : kKeyInf;
+                        const uint32_t hi = __reduce_min_sync(kFull, (uint32_t)(kk >> 32));
+                        const uint32_t lo = __reduce_min_sync(kFull, (uint32_t)(kk >> 32) == hi ? (uint32_t)kk : 0xffffffffu);
+                        nstar = ((uint64_t)hi << 32) | lo;
+                    }
+                    // 4. next expansion = min(r, best passing new key)
+                    const uint64_t nxt = nstar < key_r ? nstar : key_r;
+                    pkey = key;
+                    ppb = pb;
+                    if (nxt == kKeyInf) { ppass = pass; break; }   // no unchecked node left (pb == 0)
+                    if (nxt == key_r) {
+                        __syncwarp();
+                        if (lane == 0) C[pr] = key_r | 1ull;
+                        hint = pr + 1;
+                    } else {
+                        hint = pr >= 0 ? pr : csz;
+                        if (pass && key == nstar) pkey = key | 1ull;      // checked when it is merged
+                    }
+                    ppass = pass;
+                    u = key_id(nxt);
+                    vv = (u == spec_u) ? sv : __ldg(ix.ell + (int64_t)u * 32 + lane);
+                    if (it >= kIterCap) { status = 2; break; }
+                }
+                merge_keys(pkey, ppass, ppb);        // pending keys (overflow / cap exits)
+            }
+        }
+        // ---- outputs
+        const float inf = __int_as_float(0x7f800000);
+        if (a.cand_ids) {
+            for (int i = lane; i < ef; i += 32) {
+                a.cand_ids[q * ef + i] = i < csz ? key_id(C[i]) : -1;
+                a.cand_d[q * ef + i] = i < csz ? key_dist(C[i]) : inf;
+            }
+        }
+        for (int i = lane; i < a.k; i += 32) {
+            a.out_ids[q * a.k + i] = i < csz ? key_id(C[i]) : -1;
+            a.out_d[q * a.k + i] = i < csz ? key_dist(C[i]) : inf;
+        }
+        for (int i = lane; i < vs.count2; i += 32) vs.G[vs.log[i]] = 0u;
+        __syncwarp();
+        if (lane == 0) {
+            if (a.counters) {
+                int4 c4 = make_int4(n_exp, n_dist, n_spill, status);
+                reinterpret_cast<int4*>(a.counters)[q] = c4;
+            }
+            if (TRACE) { a.trace_nexp[q] = n_exp; a.trace_nvis[q] = n_dist; }
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace trav
 }  // namespace pa
