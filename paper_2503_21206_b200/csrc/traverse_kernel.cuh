@@ -482,6 +482,8 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
                     const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
                     bool pass = key < thresh;
                     const unsigned pb = __ballot_sync(kFull, pass);
+                    // keys entering C are likely to be expanded soon: their ELL rows go to L2 now
+                    if (pass) asm volatile("prefetch.global.L2 [%0];" :: "l"(ix.ell + (int64_t)vv * 32));
                     uint64_t nstar = kKeyInf;
                     if (pb) {
                         const uint64_t kk = pass ? key : kKeyInf;
