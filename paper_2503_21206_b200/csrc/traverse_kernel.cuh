@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
             const uint64_t key = isnew ? make_key(dist(v), v) : kKeyInf;
             const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
             const bool pass = key < thresh;
+            if (pass) asm volatile("prefetch.global.L2 [%0];" :: "l"(ix.ell + (int64_t)v * 32));
             merge_keys(key, pass, __ballot_sync(kFull, pass));
         }
         // ---- a6: pipelined Alg 1 loop
