@@ -83,8 +83,8 @@ inline float dist_full(const float* __restrict__ q, const float* __restrict__ x,
 }
 
 // Alg 1 with a sorted array C; `max_iters` < 0 ⇒ until no unchecked.
-template <class DistFn>
-void greedy(const int64_t* off, const int32_t* nb, DistFn dist, int ef, long max_iters,
+template <class DistFn, class PrefetchFn>
+void greedy(const int64_t* off, const int32_t* nb, DistFn dist, PrefetchFn prefetch, int ef, long max_iters,
             std::vector<Cand>& C, VisitedSet& vis, int64_t& n_dist) {
     long it = 0;
     while (max_iters < 0 || it < max_iters) {
@@ -95,15 +95,25 @@ void greedy(const int64_t* off, const int32_t* nb, DistFn dist, int ef, long max
         ++it;
         C[p].checked = true;
         const int32_t u = C[p].id;
-        for (int64_t e = off[u]; e < off[u + 1]; ++e) {
-            const int32_t v = nb[e];
-            if (!vis.insert(v)) continue;
-            ++n_dist;
-            Cand c{dist(v), v, false};
-            if ((int)C.size() == ef && !key_less(c, C.back())) continue;
-            auto pos = std::lower_bound(C.begin(), C.end(), c, key_less);
-            C.insert(pos, c);
-            if ((int)C.size() > ef) C.pop_back();
+        // unvisited neighbours first (stored order), their rows prefetched, then distances
+        int32_t fresh[64];
+        for (int64_t e0 = off[u]; e0 < off[u + 1];) {
+            int nf = 0;
+            for (; e0 < off[u + 1] && nf < 64; ++e0) {
+                const int32_t v = nb[e0];
+                if (!vis.insert(v)) continue;
+                fresh[nf++] = v;
+                prefetch(v);
+            }
+            for (int i = 0; i < nf; ++i) {
+                const int32_t v = fresh[i];
+                ++n_dist;
+                Cand c{dist(v), v, false};
+                if ((int)C.size() == ef && !key_less(c, C.back())) continue;
+                auto pos = std::lower_bound(C.begin(), C.end(), c, key_less);
+                C.insert(pos, c);
+                if ((int)C.size() > ef) C.pop_back();
+            }
         }
     }
 }
@@ -128,6 +138,11 @@ void run_host_stages(const HostStageArgs& a) {
             std::memcpy(qh.data(), a.qp + q * a.qp_stride, sizeof(float) * dp);
             if (dr > 0) std::memcpy(qh.data() + dp, a.qres + q * dr, sizeof(float) * dr);
             auto dfull = [&](int32_t v) { return dist_full(qh.data(), a.rotated + (int64_t)v * D, D, a.metric); };
+            const int lines = std::min(8, (D * 4 + 63) / 64);
+            auto pref = [&](int32_t v) {
+                const char* r = reinterpret_cast<const char*>(a.rotated + (int64_t)v * D);
+                for (int l = 0; l < lines; ++l) __builtin_prefetch(r + 64 * l, 0, 0);
+            };
             vis.reset();
             C.clear();
             // ---- stage ②: full δ = GPU primary δ' + residual δ (Q22)
@@ -152,11 +167,11 @@ void run_host_stages(const HostStageArgs& a) {
                 if ((int)C.size() > a.ef3) C.resize(a.ef3);
             } else {
                 if ((int)C.size() > a.ef2) C.resize(a.ef2);
-                greedy(a.sub.off, a.sub.nb, dfull, a.ef2, a.refine_iters, C, vis, my2);
+                greedy(a.sub.off, a.sub.nb, dfull, pref, a.ef2, a.refine_iters, C, vis, my2);
             }
             // ---- stage ③: Alg 1 on the full graph, carry entries unchecked, visited kept (Q23)
             for (Cand& c : C) c.checked = false;
-            greedy(a.full.off, a.full.nb, dfull, a.ef3, -1, C, vis, my3);
+            greedy(a.full.off, a.full.nb, dfull, pref, a.ef3, -1, C, vis, my3);
             for (int j = 0; j < a.k; ++j) {
                 const bool ok = j < (int)C.size();
                 a.out_ids[q * a.k + j] = ok ? C[j].id : -1;
