@@ -436,7 +436,6 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
             const uint64_t key = isnew ? make_key(dist(v), v) : kKeyInf;
             const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
             const bool pass = key < thresh;
-            if (pass) asm volatile("prefetch.global.L2 [%0];" :: "l"(ix.ell + (int64_t)v * 32));
             merge_keys(key, pass, __ballot_sync(kFull, pass));
         }
         // ---- a6: pipelined Alg 1 loop
@@ -483,8 +482,6 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
                     const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
                     bool pass = key < thresh;
                     const unsigned pb = __ballot_sync(kFull, pass);
-                    // keys entering C are likely to be expanded soon: their ELL rows go to L2 now
-                    if (pass) asm volatile("prefetch.global.L2 [%0];" :: "l"(ix.ell + (int64_t)vv * 32));
                     uint64_t nstar = kKeyInf;
                     if (pb) {
                         const uint64_t kk = pass ? key : kKeyInf;
