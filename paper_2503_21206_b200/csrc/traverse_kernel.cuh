@@ -106,6 +106,78 @@ __device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& 
     return false;   // unreachable while count2 ≤ gmask/2 (guarded by the caller)
 }
 
+// Warp-synchronous variant of visit() without shared-memory atomics (16-bit
+// atomicCAS is emulated with a 32-bit CAS loop): every pending lane probes its
+// window read-only; among lanes that picked the same empty slot the lowest one
+// writes, the others re-probe in the next round (a batch's ids are distinct, so
+// only slot collisions arbitrate).  Same table contents and results as visit().
+template <bool COMPACT>
+__device__ __forceinline__ bool visit_warp(Visited& vs, int32_t v, bool open1, bool& in_l2, uint32_t& slot,
+                                           int lane) {
+    in_l2 = false;
+    const uint32_t S = 1u << vs.log2S;
+    bool pending = v >= 0, isnew = false, to_l2 = false;
+    uint32_t P = 0, home = 0, rem = 0;
+    if (COMPACT && pending) {
+        P = perm24(v);
+        home = P >> (24 - vs.log2S);
+        rem = P & ((1u << (24 - vs.log2S)) - 1u);
+    }
+    while (__ballot_sync(kFull, pending)) {
+        int e = -1;
+        uint32_t val = 0;
+        if (pending) {
+            if constexpr (COMPACT) {
+                const volatile uint16_t* H16 = reinterpret_cast<const volatile uint16_t*>(vs.H);
+                bool done = false;
+                for (uint32_t d = 0; d < 7 && !done; ++d) {
+                    const uint32_t h = (home + d) & (S - 1);
+                    const uint16_t want = (uint16_t)((rem << 3) | d);
+                    const uint16_t cur = H16[h];
+                    if (cur == want) { pending = false; done = true; }                 // visited
+                    else if (cur == 0xFFFFu) {
+                        if (open1) { e = (int)h; val = want; }
+                        else { to_l2 = true; pending = false; }
+                        done = true;
+                    }
+                }
+                if (!done) { to_l2 = true; pending = false; }                          // window full
+            } else {
+                uint32_t h = hash1(v) >> (32 - vs.log2S);
+                for (uint32_t p = 0; p < S; ++p) {
+                    const int32_t cur = vs.H[h];
+                    if (cur == v) { pending = false; break; }
+                    if (cur == -1) {
+                        if (open1) { e = (int)h; val = (uint32_t)v; }
+                        else { to_l2 = true; pending = false; }
+                        break;
+                    }
+                    h = (h + 1) & (S - 1);
+                }
+            }
+        }
+        const unsigned peers = __match_any_sync(kFull, e);
+        if (e >= 0 && (peers & ((1u << lane) - 1u)) == 0) {
+            if constexpr (COMPACT) reinterpret_cast<volatile uint16_t*>(vs.H)[e] = (uint16_t)val;
+            else vs.H[e] = (int32_t)val;
+            pending = false;
+            isnew = true;
+        }
+        __syncwarp();
+    }
+    if (to_l2) {
+        const uint32_t tag = (uint32_t)v + 1u;
+        uint32_t g = hash2(v) & vs.gmask;
+        for (uint32_t p = 0; p <= vs.gmask; ++p) {
+            const uint32_t old = atomicCAS(&vs.G[g], 0u, tag);
+            if (old == 0u) { in_l2 = true; slot = g; isnew = true; break; }
+            if (old == tag) break;
+            g = (g + 1) & vs.gmask;
+        }
+    }
+    return isnew;
+}
+
 // Bulk prefetch of one reduced-vector row into L2 (sm_90+ cp.async.bulk.prefetch).
 __device__ __forceinline__ void prefetch_row_l2(const void* p, int bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
@@ -182,7 +254,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
             if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
             bool l2 = false;
             uint32_t slot = 0;
-            const bool isnew = v >= 0 && visit<COMPACT>(vs, v, open1, l2, slot);
+            const bool isnew = visit_warp<COMPACT>(vs, v, open1, l2, slot, lane);
             const unsigned bal = __ballot_sync(kFull, isnew);
             const unsigned bl2 = __ballot_sync(kFull, l2);
             const int nnew = __popc(bal);
@@ -406,7 +478,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
             if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
             bool l2 = false;
             uint32_t slot = 0;
-            const bool isnew = v >= 0 && visit<COMPACT>(vs, v, open1, l2, slot);
+            const bool isnew = visit_warp<COMPACT>(vs, v, open1, l2, slot, lane);
             const unsigned bal = __ballot_sync(kFull, isnew);
             const unsigned bl2 = __ballot_sync(kFull, l2);
             const int nnew = __popc(bal);
