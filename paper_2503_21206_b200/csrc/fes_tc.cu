@@ -425,6 +425,38 @@ __device__ __forceinline__ void warp_bitonic_smem(uint64_t* a, int n, int lane) 
         }
 }
 
+// Ascending bitonic sort of n = 32·K 64-bit keys held in registers, element
+// i = a·32 + lane in t[a]: partners at distance ≥ 32 are in the same lane.
+template <int K>
+__device__ __forceinline__ void warp_bitonic_regs(uint64_t (&t)[K], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    const int b = a ^ (j >> 5);
+                    if (b > a) {
+                        const bool up = ((a * 32 + lane) & k) == 0;
+                        const uint64_t x = t[a], y = t[b];
+                        if ((x > y) == up) { t[a] = y; t[b] = x; }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    const uint64_t y = shfl_xor64(t[a], j);
+                    const bool up = ((a * 32 + lane) & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    const uint64_t mn = t[a] < y ? t[a] : y, mx = t[a] < y ? y : t[a];
+                    t[a] = (lower == up) ? mn : mx;
+                }
+            }
+        }
+    }
+}
+
 template <int KPMAX, int SMAX>
 __global__ void __launch_bounds__(128) k_fes_select2(FesParams p, int64_t m) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -497,7 +529,18 @@ __global__ void __launch_bounds__(128) k_fes_select2(FesParams p, int64_t m) {
             M += add;
         }
         __syncwarp();
-        if (!overflow) {
+        if (!overflow && M <= 128) {                  // common case: sort in registers
+            uint64_t t4[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) t4[a] = a * 32 + lane < M ? buf[a * 32 + lane] : kKeyInf;
+            warp_bitonic_regs<4>(t4, lane);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int j = a * 32 + lane;
+                if (j < E) p.entries[(int64_t)q * E + j] = j < M ? key_id(t4[a]) : -1;
+            }
+            for (int j = 128 + lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = -1;
+        } else if (!overflow) {
             int n2 = 32;
             while (n2 < M) n2 <<= 1;
             for (int i = M + lane; i < n2; i += 32) buf[i] = kKeyInf;
