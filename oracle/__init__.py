@@ -42,7 +42,7 @@ class OrcOpts(C.Structure):
     _fields_ = [("k", C.c_int32), ("ef1", C.c_int32), ("ef2", C.c_int32), ("ef3", C.c_int32),
                 ("entries", C.c_int32), ("width", C.c_int32), ("refine_iters", C.c_int32),
                 ("stages", C.c_int32), ("flags", C.c_uint32), ("threads", C.c_int32),
-                ("trace_cap", C.c_int32)]
+                ("trace_cap", C.c_int32), ("bloom_log2", C.c_int32), ("use_bloom", C.c_int32)]
 
 
 class OrcOut(C.Structure):
@@ -110,14 +110,16 @@ def make_index(inst: dict):
 
 
 def search(inst: dict, queries=None, k: int = 10, ef: int = 64, stages: int = 1, flags: int = 0,
-           threads: int = 0, trace_cap: int = 0, **budgets) -> dict:
-    """Run O1-O9 over `queries` (default inst['queries']).  Returns numpy arrays."""
+           threads: int = 0, trace_cap: int = 0, bloom_log2=None, **budgets) -> dict:
+    """Run O1-O9 over `queries` (default inst['queries']).  Returns numpy arrays.
+    bloom_log2 = s selects the O13 bloom-filter visited set in stage ① (3 × 2^s bits)."""
     ix, keep = make_index(inst)
     Q = _c(inst["queries"] if queries is None else queries, np.float32)
     m = Q.shape[0]
     b = default_budgets(k, ef)
     b.update(budgets)
-    o = OrcOpts(k=k, stages=stages, flags=flags, threads=threads, trace_cap=trace_cap, **b)
+    o = OrcOpts(k=k, stages=stages, flags=flags, threads=threads, trace_cap=trace_cap,
+                bloom_log2=0 if bloom_log2 is None else int(bloom_log2), use_bloom=0 if bloom_log2 is None else 1, **b)
     E, ef1 = b["entries"], b["ef1"]
     res = dict(ids=np.full((m, k), -1, np.int32), d=np.zeros((m, k)), cell=np.zeros(m, np.int32),
                entries=np.zeros((m, E), np.int32), entries_d=np.zeros((m, E)),

@@ -26,6 +26,13 @@
 //   O10 toggles               no-FES / no-stage1 / no-stage2
 //   O11 brute force           exact top-k by (δ, id) over an id set
 //   O12 recall@k              |ret_k ∩ gt_k| / k  (+ tie-aware variant)            P:L657; Q25
+//   O13 bloom visited (opt.)  stage-① visited set as a partitioned bloom filter   P:L392-395 (§4.3)
+//                             (3 segments × 2^s bits, segment j hashes v to
+//                             ((uint32)v · A_j mod 2^32) >> (32 − s)); a neighbour
+//                             is "visited" iff its 3 bits are set, else its bits
+//                             are set (test-then-set, in stored order).  Entries
+//                             enter C unconditionally and set their bits.  Stages
+//                             ②③ keep EXACT sets.  DESIGN.md reading Q17b.
 //
 // Parity status: every function here is pinned by tests/test_oracle.py (see its
 // module docstring for the pin of each O-step).
@@ -65,6 +72,8 @@ struct OrcOpts {
     uint32_t flags;                 // 1 = no FES, 2 = no stage ②, 4 = no stage ①  (O10)
     int32_t threads;                // 0 = hardware_concurrency
     int32_t trace_cap;              // per-query capacity of stage-① traces (0 = none)
+    int32_t bloom_log2;             // O13: 0 = exact stage-① visited set; s ≥ 0 bits per segment = 2^s
+    int32_t use_bloom;              // 1 = O13 bloom filter in stage ① (bloom_log2 = s, may be 0)
 };
 
 struct OrcOut {
@@ -110,6 +119,40 @@ struct Trace {
     std::vector<int32_t> expand, visit;
 };
 
+// Visited set of Alg 1 (l.6-7): exact (std::unordered_set) or, for stage ① on
+// request, the O13 partitioned bloom filter.  insert(v) returns true iff v was
+// not (believed) visited, and marks it visited.
+struct VisitedSet {
+    bool bloom = false;
+    int32_t s = 0;                                   // bits per segment = 2^s
+    std::unordered_set<int32_t> exact;
+    std::vector<uint8_t> bits[3];                    // one byte per bit: plain, not fast
+    static uint32_t bloom_bit(int32_t v, int j, int32_t s) {
+        static const uint32_t A[3] = {0x9E3779B1u, 0x85EBCA77u, 0xC2B2AE3Du};
+        uint32_t h = (uint32_t)v * A[j];             // mod 2^32
+        return s == 0 ? 0u : (h >> (32 - s));
+    }
+    void make_bloom(int32_t s_) {
+        bloom = true;
+        s = s_;
+        for (auto& b : bits) b.assign((size_t)1 << s, 0);
+    }
+    bool test(int32_t v) const {                     // all 3 bits set?
+        for (int j = 0; j < 3; ++j)
+            if (!bits[j][bloom_bit(v, j, s)]) return false;
+        return true;
+    }
+    void set(int32_t v) {
+        for (int j = 0; j < 3; ++j) bits[j][bloom_bit(v, j, s)] = 1;
+    }
+    bool insert(int32_t v) {
+        if (!bloom) return exact.insert(v).second;
+        if (test(v)) return false;                   // visited, or a false positive (§4.3)
+        set(v);
+        return true;
+    }
+};
+
 // ------------------------------------------------------ O6 Alg 1
 // Runs at most `max_iters` outer iterations (−1 = until no unchecked node).
 // Alg 1: u ← first unchecked node in C (l.5); for unvisited v ∈ N(u) (l.6):
@@ -118,7 +161,7 @@ struct Trace {
 // rows concatenated in key order (w = 1 is Alg 1 exactly).
 template <class DistFn>
 void greedy(const int64_t* off, const int32_t* nb, DistFn dist, int32_t ef, int32_t w,
-            long max_iters, std::vector<Cand>& C, std::unordered_set<int32_t>& vis,
+            long max_iters, std::vector<Cand>& C, VisitedSet& vis,
             int64_t& n_exp, int64_t& n_dist, Trace* tr) {
     long it = 0;
     while (max_iters < 0 || it < max_iters) {
@@ -138,7 +181,7 @@ void greedy(const int64_t* off, const int32_t* nb, DistFn dist, int32_t ef, int3
             if (tr) tr->expand.push_back(u);
             for (int64_t e = off[u]; e < off[u + 1]; ++e) {   // l.6, stored order
                 int32_t v = nb[e];
-                if (vis.insert(v).second) {                    // l.7 (unvisited → visited)
+                if (vis.insert(v)) {                           // l.7 (unvisited → visited)
                     fresh.push_back(Cand{dist(v), v, false});  // l.8
                     ++n_dist;
                     if (tr) tr->visit.push_back(v);
@@ -207,9 +250,11 @@ void search_one(const OrcIndex& ix, const float* q, const OrcOpts& o, const OrcO
     Trace tr;
     Trace* trp = o.trace_cap > 0 ? &tr : nullptr;
     std::vector<Cand> C = ent;
-    std::unordered_set<int32_t> vis;
+    VisitedSet vis;
+    if (o.use_bloom) vis.make_bloom(o.bloom_log2);    // O13 (stage ① only)
     for (const Cand& c : ent) {
-        vis.insert(c.id);
+        if (vis.bloom) vis.set(c.id);                  // entries enter C unconditionally (O13)
+        else vis.insert(c.id);
         if (trp) trp->visit.push_back(c.id);
     }
     local[kNDist1] = (int64_t)ent.size();
@@ -243,7 +288,7 @@ void search_one(const OrcIndex& ix, const float* q, const OrcOpts& o, const OrcO
     } else {
         // ---- O8 stage ② residual refinement
         std::vector<Cand> C2;
-        std::unordered_set<int32_t> vis2;
+        VisitedSet vis2;                                        // exact
         for (const Cand& c : cand1) {                           // full δ = primary + residual
             C2.push_back(Cand{dfull(c.id), c.id, false});
             vis2.insert(c.id);
@@ -286,7 +331,7 @@ void parallel_for(int64_t m, int32_t threads, F f) {
 
 extern "C" {
 
-int orc_version() { return 1; }
+int orc_version() { return 2; }
 
 // O1 alone: q̂[m][D] = q·V in fp64.
 void orc_project(const float* Q, int64_t m, int32_t D, const float* V, double* Qh) {

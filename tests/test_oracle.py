@@ -312,3 +312,84 @@ def test_multithread_equals_single_thread(s1):
     b = orc.search(s1, k=10, ef=32, stages=1, threads=8)
     for key in ("ids", "d", "cand1_ids", "counters", "entries"):
         assert np.array_equal(a[key], b[key])
+
+
+# ------------------------------------------------------------ O13 bloom -----
+# The stage-① visited set as the paper's bloom filter,
+# partitioned into 3 segments of 2^s bits (reading Q17b).
+def _bloom_inst(seed=70):
+    return tiny_instance(n=600, D=12, dp=6, R=10, m=16, seed=seed, member_ratio=0.8)
+
+
+def test_bloom_huge_filter_equals_exact_visited():
+    """With 3 × 2^20 bits and ≤ 600 inserts a false positive has probability
+    < 1e-9 per test, so the bloom search must reproduce the exact-set search
+    (itself pinned by the goldens / brute force above) trace for trace."""
+    inst = _bloom_inst()
+    a = orc.search(inst, k=10, ef=24, trace_cap=4096, entries=6)
+    b = orc.search(inst, k=10, ef=24, trace_cap=4096, entries=6, bloom_log2=20)
+    for key in ("cand1_ids", "cand1_d", "trace_expand", "trace_visit", "trace_nexp", "trace_nvis", "n_dist1"):
+        np.testing.assert_array_equal(a[key], b[key])
+
+
+def test_bloom_all_positive_filter_keeps_only_entries():
+    """a filter that answers 'visited' for everything (s = 0: one bit per
+    segment, set by the first entry) leaves C = the entries — the same list as
+    the no-stage-① toggle (pinned above)."""
+    inst = _bloom_inst(71)
+    b = orc.search(inst, k=5, ef=16, entries=8, trace_cap=256, bloom_log2=0)
+    t = orc.search(inst, k=5, ef=16, entries=8, flags=orc.NO_STAGE1)
+    np.testing.assert_array_equal(b["cand1_ids"], t["cand1_ids"])
+    assert np.all(b["n_dist1"] == 8) and np.all(b["trace_nvis"] == 8)
+
+
+def test_bloom_no_false_negatives_and_fp_rate():
+    """No false negatives: no id is ever visited twice.  False-positive
+    rate: replaying each trace against the true visited set, a fresh neighbour
+    tested after n inserts is skipped with probability (1 − (1 − 2^−s)^n)^3 for
+    three independent uniform segment hashes; the observed skip count must match
+    the sum of these probabilities within 5σ (a test that required any ONE bit,
+    or a single shared segment, would be off by many σ)."""
+    inst = _bloom_inst(72)
+    s = 7
+    res = orc.search(inst, k=10, ef=32, trace_cap=8192, entries=6, bloom_log2=s)
+    off, nb = inst["sub_offsets"], inst["sub_neighbors"]
+    exp_fp, var, obs, tests = 0.0, 0.0, 0, 0
+    for q in range(inst["queries"].shape[0]):
+        vis = list(res["trace_visit"][q][:res["trace_nvis"][q]])
+        assert len(set(vis)) == len(vis)                                   # no revisits
+        E = 6
+        T = set(vis[:E])
+        nxt = E
+        for u in res["trace_expand"][q][:res["trace_nexp"][q]]:
+            for v in nb[off[u]:off[u + 1]]:
+                if v in T:
+                    continue
+                p = (1.0 - (1.0 - 2.0 ** -s) ** len(T)) ** 3
+                tests += 1
+                exp_fp += p
+                var += p * (1 - p)
+                if nxt < len(vis) and vis[nxt] == v:
+                    T.add(v)
+                    nxt += 1
+                else:
+                    obs += 1                                               # skipped: false positive
+        assert nxt == len(vis)
+    assert tests > 2000 and exp_fp > 20
+    assert abs(obs - exp_fp) <= 5 * np.sqrt(var), (obs, exp_fp, var)
+
+
+def test_bloom_stage1_invariants():
+    """I1, I2, I7 (C = the ef best of what was visited), I8, I9 hold under FPs."""
+    inst = _bloom_inst(73)
+    ef = 16
+    res = orc.search(inst, k=5, ef=ef, trace_cap=4096, entries=5, bloom_log2=7)
+    Qh = orc.project(inst["queries"], inst["basis"])
+    for q in range(inst["queries"].shape[0]):
+        vis = res["trace_visit"][q][:res["trace_nvis"][q]]
+        assert res["n_dist1"][q] == len(vis)
+        c = res["cand1_ids"][q]
+        c = c[c >= 0]
+        dd = ((inst["reduced"][vis].astype(np.float64) - Qh[q, :6]) ** 2).sum(1)
+        assert list(c) == list(np.asarray(vis)[np.lexsort((vis, dd))[:ef]])
+        assert np.all(inst["member_flags"][c] == 1)
