@@ -167,18 +167,18 @@ def run_reference(args, rank, world):
     if not ef:                       # same operating-point rule as the GPU arm, on a sample
         probe = min(len(Q), 500)
         for e in EF_SWEEP:
-            rr = orc.search(inst, queries=Q[:probe], k=cfg.k, ef=e, stages=1)
+            rr = orc.search(inst, queries=Q[:probe], k=cfg.k, ef=e, stages=1, bloom_log2=args.bloom or None)
             if recall_at(rr["ids"], inst["gt_sub_ids"][:probe], cfg.k) >= TARGET_RECALL:
                 ef = e
                 break
         ef = ef or EF_SWEEP[-1]
     for _ in range(args.warmup):
-        orc.search(inst, queries=Q[:min(sample, 64)], k=cfg.k, ef=ef, stages=1)
+        orc.search(inst, queries=Q[:min(sample, 64)], k=cfg.k, ef=ef, stages=1, bloom_log2=args.bloom or None)
     times = []
     for s in range(args.steps):
         qs = Q[(s * sample) % len(Q):][:sample]
         t = time.perf_counter()
-        r = orc.search(inst, queries=qs, k=cfg.k, ef=ef, stages=1)
+        r = orc.search(inst, queries=qs, k=cfg.k, ef=ef, stages=1, bloom_log2=args.bloom or None)
         times.append(time.perf_counter() - t)
     qps = sample * len(times) / sum(times)
     rec = recall_at(r["ids"], inst["gt_sub_ids"][(s * sample) % len(Q):][:sample], cfg.k)
@@ -188,7 +188,8 @@ def run_reference(args, rank, world):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "ef": ef, "k": cfg.k, "sample_queries_per_step": sample},
             "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{sample} queries per step of {cfg.name}, stage 1, ef={ef}"},
+                             "sample": f"{sample} queries per step of {cfg.name}, stage 1, ef={ef}"
+                                       + (f", bloom 3x2^{args.bloom}" if args.bloom else "")},
             "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "recall_at_10_sample": rec}
     print(json.dumps(line), flush=True)
@@ -229,7 +230,7 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
 
     def step(ef):
-        ix.search_device(qd, k, ef, out_i, out_d, stream=stream.cuda_stream)
+        ix.search_device(qd, k, ef, out_i, out_d, stream=stream.cuda_stream, bloom_log2=args.bloom)
 
     # ---- operating point: smallest ef with Recall@10 (vs GT_sub) ≥ 0.90
     sweep = []
@@ -280,6 +281,7 @@ def run_ours(args, rank, world, local_rank):
             acc["fes"].append(st["ms_fes"])
             acc["launches"] += st["kernel_launches"]
             acc["bytes"] = st["sum_n_exp"] * 4 * ell_w + st["sum_n_dist"] * row_bytes
+            acc["n_exp"], acc["n_dist"] = st["sum_n_exp"], st["sum_n_dist"]
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -300,46 +302,64 @@ def run_ours(args, rank, world, local_rank):
     rec_full = recall_at(out_i.cpu().numpy(), inst["gt_ids"], k)
     qps = m * world / (ms / 1e3)
 
-    # ---- NEXT-f1 variant: the same search with binary16-stored reduced rows
-    f1 = None
-    if args.reduced == "fp32" and not args.no_f1:
-        ix16 = pa.Index.from_instance(inst, device=local_rank, reduced_fp16=True)
+    # ---- NEXT-f1 variants: binary16-stored reduced rows and/or the paper's bloom
+    # visited set, each at its own smallest ef with Recall@10 (GT_sub) >= 0.90
+    def variant(name, what, fp16, bloom):
+        ixv = pa.Index.from_instance(inst, device=local_rank, reduced_fp16=fp16) if fp16 else ix
 
-        def step16(e):
-            ix16.search_device(qd, k, e, out_i, out_d, stream=stream.cuda_stream)
-        ef16 = None
+        def stepv(e):
+            ixv.search_device(qd, k, e, out_i, out_d, stream=stream.cuda_stream, bloom_log2=bloom)
+        efv = None
         for e in EF_SWEEP:
-            step16(e)
+            stepv(e)
             torch.cuda.synchronize()
             if recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k) >= TARGET_RECALL:
-                ef16 = e
+                efv = e
                 break
-        ef16 = ef16 or EF_SWEEP[-1]
+        efv = efv or EF_SWEEP[-1]
         if world > 1:
-            t = torch.tensor([ef16], device=dev)
+            t = torch.tensor([efv], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ef16 = int(t.item())
-        v = timed(step16, ix16, ef16, True)
-        r16 = recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k)
+            efv = int(t.item())
+        v = timed(stepv, ixv, efv, fp16)
+        rv = recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k)
         pk, _ = measured_peaks()
         ach = v["bytes"] / (v["trav_ms"] / 1e3) / 1e9
-        f1 = {"what": "NEXT-f1: reduced rows stored as binary16 (rounded once at build; fp32 arithmetic; "
-                      "parity vs the oracle on the same rounded values)",
-              "value": round(m * world / (v["ms"] / 1e3), 1), "unit": "queries/s", "ef": ef16,
-              "recall_at_10_gt_sub": round(r16, 4), "ms_per_step": round(v["ms"], 4),
-              "traverse_ms": round(v["trav_ms"], 4), "alg_bytes_per_launch": v["bytes"],
-              "roofline_frac": round(ach / pk, 4), "achieved_gbs": round(ach, 1)}
-        ix16.close()
+        if fp16:
+            ixv.close()
+        return {"what": what, "reduced_storage": "fp16" if fp16 else "fp32", "bloom_log2": bloom,
+                "value": round(m * world / (v["ms"] / 1e3), 1), "unit": "queries/s", "ef": efv,
+                "recall_at_10_gt_sub": round(rv, 4), "ms_per_step": round(v["ms"], 4),
+                "traverse_ms": round(v["trav_ms"], 4), "alg_bytes_per_launch": v["bytes"],
+                "n_dist_per_q": v["n_dist"] / m, "n_exp_per_q": v["n_exp"] / m,
+                "roofline_frac": round(ach / pk, 4), "achieved_gbs": round(ach, 1)}
+
+    variants = {}
+    if not args.no_f1:
+        want = [x for x in args.variants.split(",") if x]
+        specs = {
+            "fp16": ("NEXT-f1: reduced rows stored as binary16 (rounded once at build; fp32 arithmetic; "
+                     "parity vs the oracle on the same rounded values)", True, 0),
+            "bloom": (f"NEXT-f1: the paper's shared-memory bloom visited set (P:L392-395), 3 x 2^{args.bloom_bits} "
+                      "bits per query; parity vs the oracle's O13 mode", False, args.bloom_bits),
+            "bloom_fp16": ("NEXT-f1: bloom visited set + binary16 rows", True, args.bloom_bits),
+        }
+        for name in want:
+            if name in specs and not (name == "fp16" and args.reduced == "fp16") and \
+                    not (name == "bloom" and args.bloom):
+                variants[name] = variant(name, *specs[name])
+                log(f"[rank {rank}] variant {name}: {variants[name]['value']:.0f} q/s ef={variants[name]['ef']} "
+                    f"trav {variants[name]['traverse_ms']:.3f} ms")
 
     # ---- e2e through the public host API: pinned host queries in, host results out
     hq = torch.from_numpy(inst["queries"]).pin_memory()
     ho = (torch.empty(m, k, dtype=torch.int32).pin_memory(), torch.empty(m, k, dtype=torch.float32).pin_memory())
     for _ in range(2):
-        ix.search(hq, k=k, ef=ef, out=ho)
+        ix.search(hq, k=k, ef=ef, out=ho, bloom_log2=args.bloom)
     e2e_t = []
     for _ in range(max(3, args.steps)):
         t = time.perf_counter()
-        ix.search(hq, k=k, ef=ef, out=ho)
+        ix.search(hq, k=k, ef=ef, out=ho, bloom_log2=args.bloom)
         e2e_t.append(time.perf_counter() - t)
     e2e_s = sum(e2e_t) / len(e2e_t)
     if world > 1:
@@ -371,6 +391,7 @@ def run_ours(args, rank, world, local_rank):
                        "recall_at_10_gt_sub": round(rec, 4), "recall_at_10_full_gt_gpu_only": round(rec_full, 4),
                        "l2": "flushed between steps (512 MB write), per-step CUDA events",
                        "reduced_storage": args.reduced,
+                       "visited": f"bloom 3x2^{args.bloom} bits" if args.bloom else "exact",
                        "parallelism": f"query-sharded x{world}, replicated index"},
             "ef_sweep": sweep,
             "roofline": {"bound": "hbm", "kernel": "k_traverse", "achieved": round(achieved, 1),
@@ -385,7 +406,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": m * cfg.D * 4,
                     "d2h_bytes_per_step": m * k * 8},
             "end_to_end_full": full,
-            "f1_fp16_storage": f1,
+            "f1_variants": variants,
             "gpu_launches": launches,
             "clocks": clocks,
         }
@@ -402,9 +423,9 @@ def measure_full(ix, inst, cfg, args, rank):
     sweep = []
     hq = inst["queries"]
     for ef in (16, 32, 64, 128, 192, 256):
-        ix.search(hq, k=k, ef=ef, stages=pa.PA_STAGES_FULL)              # warm-up (pinned buffers, pools)
+        ix.search(hq, k=k, ef=ef, stages=pa.PA_STAGES_FULL, bloom_log2=args.bloom)              # warm-up (pinned buffers, pools)
         t = time.perf_counter()
-        ids, _ = ix.search(hq, k=k, ef=ef, stages=pa.PA_STAGES_FULL)
+        ids, _ = ix.search(hq, k=k, ef=ef, stages=pa.PA_STAGES_FULL, bloom_log2=args.bloom)
         dt = time.perf_counter() - t
         rec = recall_at(ids, inst["gt_ids"], k)
         st = ix.stats()
@@ -427,14 +448,15 @@ def cpu_baseline(inst, cfg, ef, args):
     Q = inst["queries"]
     cal = Q[:64]
     t = time.perf_counter()
-    orc.search(inst, queries=cal, k=cfg.k, ef=ef, stages=1)
+    orc.search(inst, queries=cal, k=cfg.k, ef=ef, stages=1, bloom_log2=args.bloom or None)
     per_q = (time.perf_counter() - t) / len(cal)
     n = int(min(len(Q), max(256, args.cpu_seconds / max(per_q, 1e-6))))
     t = time.perf_counter()
-    r = orc.search(inst, queries=Q[:n], k=cfg.k, ef=ef, stages=1)
+    r = orc.search(inst, queries=Q[:n], k=cfg.k, ef=ef, stages=1, bloom_log2=args.bloom or None)
     dt = time.perf_counter() - t
     return {"value": round(n / dt, 1), "unit": "queries/s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"first {n} queries of {cfg.name}, stage 1 (projection+FES+traversal), ef={ef}, fp64",
+            "sample": f"first {n} queries of {cfg.name}, stage 1 (projection+FES+traversal), ef={ef}, fp64"
+                      + (f", bloom 3x2^{args.bloom}" if args.bloom else ""),
             "recall_at_10_gt_sub": round(recall_at(r["ids"], inst["gt_sub_ids"][:n], cfg.k), 4)}
 
 
@@ -457,6 +479,10 @@ def main():
     ap.add_argument("--repeat-queries", type=int, default=1, help="experiment only: tile the query batch R times")
     ap.add_argument("--reduced", default="fp32", choices=["fp32", "fp16"],
                     help="storage of the reduced rows on the GPU (fp16 = NEXT-f1; parity on the rounded values)")
+    ap.add_argument("--bloom", type=int, default=0,
+                    help="headline path with the bloom visited set of 3 x 2^BLOOM bits (0 = exact set)")
+    ap.add_argument("--bloom-bits", type=int, default=12, help="bloom size of the bloom variants")
+    ap.add_argument("--variants", default="fp16,bloom,bloom_fp16", help="NEXT-f1 variants measured beside the headline")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -104,6 +104,12 @@ typedef struct {
     uint32_t flags;          /* PA_NO_* ablation toggles                                       */
     int32_t hash_slots_log2; /* visited-hash smem slots = 2^this (0 ⇒ auto); test hook for spill */
     int32_t host_threads;    /* threads for stages ②③ (0 ⇒ env PILOTANN_HOST_THREADS or all cores) */
+    int32_t bloom_log2;      /* NEXT-f1, the paper's own visited set: 0 ⇒ EXACT visited set;
+                                s in 7..16 ⇒ stage ① tracks visited nodes in a shared-memory bloom filter of
+                                3 segments × 2^s bits (segment j: bit ((uint32)v·A_j) >> (32−s), A = 0x9E3779B1,
+                                0x85EBCA77, 0xC2B2AE3D).  False positives skip nodes (stages ②③ keep exact
+                                sets and re-visit); results then match the oracle's O13 mode.
+                                Requires max_degree ≤ 32 (PA_ENOTSUP otherwise); other values PA_EINVAL. */
 } pa_search_opts;
 
 /* Optional per-query debug/trace outputs of stage ① (DEVICE pointers, may be

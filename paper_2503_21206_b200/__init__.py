@@ -51,7 +51,8 @@ class BuildParams(C.Structure):
 class SearchOpts(C.Structure):
     _fields_ = [("stages", C.c_int32), ("ef1", C.c_int32), ("ef2", C.c_int32), ("ef3", C.c_int32),
                 ("entries", C.c_int32), ("width", C.c_int32), ("refine_iters", C.c_int32),
-                ("flags", C.c_uint32), ("hash_slots_log2", C.c_int32), ("host_threads", C.c_int32)]
+                ("flags", C.c_uint32), ("hash_slots_log2", C.c_int32), ("host_threads", C.c_int32),
+                ("bloom_log2", C.c_int32)]
 
 
 class Debug(C.Structure):
@@ -123,10 +124,10 @@ def _ptr(a):
 
 
 def make_opts(stages=PA_STAGES_GPU, ef1=0, ef2=0, ef3=0, entries=0, width=0, refine_iters=0, flags=0,
-              hash_slots_log2=0, host_threads=0) -> SearchOpts:
+              hash_slots_log2=0, host_threads=0, bloom_log2=0) -> SearchOpts:
     return SearchOpts(stages=stages, ef1=ef1, ef2=ef2, ef3=ef3, entries=entries, width=width,
                       refine_iters=refine_iters, flags=flags, hash_slots_log2=hash_slots_log2,
-                      host_threads=host_threads)
+                      host_threads=host_threads, bloom_log2=bloom_log2)
 
 
 class Index:

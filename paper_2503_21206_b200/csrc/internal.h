@@ -37,6 +37,7 @@ struct SearchArgs {
     int32_t k = 10, ef = 64, E = 64;
     uint32_t flags = 0;
     int32_t hash_log2 = 12;
+    int32_t bloom_log2 = 0;        // > 0: stage-① visited set = bloom filter, 3 segments × 2^this bits (NEXT-f1)
     const float* q = nullptr;      // [m][dim]
     float* qp = nullptr;           // [m][rdim_pad]  projected q'
     float* qres = nullptr;         // [m][dim − rdim] (optional) residual projection for host stages

@@ -210,7 +210,7 @@ pa_status ensure_spill(pa_index* ix, int64_t warps) {
 }
 
 struct Resolved {
-    int32_t stages, ef1, ef2, ef3, E, width, refine, hash_log2, threads;
+    int32_t stages, ef1, ef2, ef3, E, width, refine, hash_log2, threads, bloom_log2;
     uint32_t flags;
 };
 
@@ -230,6 +230,9 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, i
     r->flags = o->flags;
     r->hash_log2 = o->hash_slots_log2 ? o->hash_slots_log2 : default_hash_log2(r->ef1, n);
     r->threads = threads_default(o->host_threads);
+    r->bloom_log2 = o->bloom_log2;
+    if (r->bloom_log2 != 0 && (r->bloom_log2 < 7 || r->bloom_log2 > 16))
+        return fail(PA_EINVAL, "bloom_log2 = %d (0 or 7..16)", r->bloom_log2);
     if (r->ef1 > 256 || r->ef2 > 256 || r->ef3 > 256) return fail(PA_EINVAL, "ef > 256");
     if (r->ef1 < 1 || r->ef2 < 1 || r->ef3 < 1 || r->E < 1 || r->E > 1024) return fail(PA_EINVAL, "bad ef/entries");
     if (r->stages == PA_STAGES_GPU && k > r->ef1) return fail(PA_EINVAL, "k = %d > ef1 = %d", k, r->ef1);
@@ -248,6 +251,8 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     const auto& dd = ix->dev;
     pa::SearchArgs a;
     a.m = m; a.k = k; a.ef = r.ef1; a.E = r.E; a.flags = r.flags; a.hash_log2 = r.hash_log2;
+    a.bloom_log2 = r.bloom_log2;
+    if (a.bloom_log2 > 0 && dd.ell_w != 32) return fail(PA_ENOTSUP, "bloom visited set needs max_degree <= 32");
     a.q = d_q; a.qp = ix->qp + row0 * dd.rdim_pad;
     a.qres = want_qres ? ix->qres + row0 * std::max(1, dd.dim - dd.rdim) : nullptr;
     a.cell = (dbg && dbg->cell) ? dbg->cell : ix->cell + row0;

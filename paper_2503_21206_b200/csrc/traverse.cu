@@ -23,6 +23,10 @@ void* traverse_pick_pipe_1cf(int ef, int d, bool trace);
 void* traverse_pick_pipe_1ch(int ef, int d, bool trace);
 void* traverse_pick_pipe_1wf(int ef, int d, bool trace);
 void* traverse_pick_pipe_1wh(int ef, int d, bool trace);
+void* traverse_pick_pipe_0bf(int ef, int d, bool trace);
+void* traverse_pick_pipe_0bh(int ef, int d, bool trace);
+void* traverse_pick_pipe_1bf(int ef, int d, bool trace);
+void* traverse_pick_pipe_1bh(int ef, int d, bool trace);
 
 constexpr int kTW = 4;
 }  // namespace trav
@@ -37,6 +41,13 @@ bool use_compact(const DevIndex& ix, const SearchArgs& a) {
 }
 void* pick(const DevIndex& ix, const SearchArgs& a) {
     const bool cp = use_compact(ix, a), tr = a.trace_cap > 0;
+    if (a.bloom_log2 > 0) {                                          // bloom visited set: pipelined kernel only
+        if (ix.ell_w != 32) return nullptr;
+        const bool h = ix.reduced_h != nullptr;
+        const int d = h ? ix.rdim_h : ix.rdim_pad;
+        if (ix.metric == 0) return h ? trav::traverse_pick_pipe_0bh(a.ef, d, tr) : trav::traverse_pick_pipe_0bf(a.ef, d, tr);
+        return h ? trav::traverse_pick_pipe_1bh(a.ef, d, tr) : trav::traverse_pick_pipe_1bf(a.ef, d, tr);
+    }
     const char* ve = std::getenv("PA_TRAVERSE");
     if (ix.ell_w == 32 && !(ve && !std::strcmp(ve, "v1"))) {        // software-pipelined kernel
         const bool h = ix.reduced_h != nullptr;
@@ -60,13 +71,16 @@ void* pick(const DevIndex& ix, const SearchArgs& a) {
 
 size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
     const size_t efp = (size_t)((a.ef + 1) & ~1);
-    size_t per_warp = efp * 8 + (size_t)ix.qlen * 4 + ((size_t)(use_compact(ix, a) ? 2 : 4) << a.hash_log2);
+    const size_t vis = a.bloom_log2 > 0 ? ((size_t)3 << (a.bloom_log2 - 3))
+                                        : ((size_t)(use_compact(ix, a) ? 2 : 4) << a.hash_log2);
+    size_t per_warp = efp * 8 + (size_t)ix.qlen * 4 + vis;
     return per_warp * kTW;
 }
 }  // namespace
 
 int traverse_max_warps(const DevIndex& ix, const SearchArgs& a) {
     void* fn = pick(ix, a);
+    if (!fn) return 0;
     size_t smem = smem_bytes(ix, a);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = 0, dev = 0, sms = 0;

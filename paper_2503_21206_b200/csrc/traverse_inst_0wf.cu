@@ -5,45 +5,45 @@
 namespace pa {
 namespace trav {
 namespace {
-template <int METRIC, bool COMPACT, int SMAX>
+template <int METRIC, int VIS, int SMAX>
 void* pick4(int d, bool trace) {
-    if (trace) return (void*)k_traverse<METRIC, COMPACT, SMAX, 0, true, false>;
+    if (trace) return (void*)k_traverse<METRIC, VIS, SMAX, 0, true, false>;
     switch (d) {
-        case 32: return (void*)k_traverse<METRIC, COMPACT, SMAX, 8, false, false>;
-        case 48: return (void*)k_traverse<METRIC, COMPACT, SMAX, 12, false, false>;
-        case 64: return (void*)k_traverse<METRIC, COMPACT, SMAX, 16, false, false>;
-        case 128: return (void*)k_traverse<METRIC, COMPACT, SMAX, 32, false, false>;
-        default: return (void*)k_traverse<METRIC, COMPACT, SMAX, 0, false, false>;
+        case 32: return (void*)k_traverse<METRIC, VIS, SMAX, 8, false, false>;
+        case 48: return (void*)k_traverse<METRIC, VIS, SMAX, 12, false, false>;
+        case 64: return (void*)k_traverse<METRIC, VIS, SMAX, 16, false, false>;
+        case 128: return (void*)k_traverse<METRIC, VIS, SMAX, 32, false, false>;
+        default: return (void*)k_traverse<METRIC, VIS, SMAX, 0, false, false>;
     }
 }
-template <int METRIC, bool COMPACT, int SMAX>
+template <int METRIC, int VIS, int SMAX>
 void* pick4p(int d, bool trace) {
-    if (trace) return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 0, true, false>;
+    if (trace) return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 0, true, false>;
     switch (d) {
-        case 32: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 8, false, false>;
-        case 48: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 12, false, false>;
-        case 64: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 16, false, false>;
-        case 128: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 32, false, false>;
-        default: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 0, false, false>;
+        case 32: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 8, false, false>;
+        case 48: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 12, false, false>;
+        case 64: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 16, false, false>;
+        case 128: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 32, false, false>;
+        default: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 0, false, false>;
     }
 }
 }  // namespace
 
 void* traverse_pick_0wf(int ef, int d, bool trace) {
     constexpr int METRIC = 0;
-    constexpr bool COMPACT = false;
-    if (ef <= 64) return pick4<METRIC, COMPACT, 2>(d, trace);
-    if (ef <= 96) return pick4<METRIC, COMPACT, 3>(d, trace);
-    if (ef <= 128) return pick4<METRIC, COMPACT, 4>(d, trace);
-    return pick4<METRIC, COMPACT, 8>(d, trace);
+    constexpr int VIS = 0;
+    if (ef <= 64) return pick4<METRIC, VIS, 2>(d, trace);
+    if (ef <= 96) return pick4<METRIC, VIS, 3>(d, trace);
+    if (ef <= 128) return pick4<METRIC, VIS, 4>(d, trace);
+    return pick4<METRIC, VIS, 8>(d, trace);
 }
 void* traverse_pick_pipe_0wf(int ef, int d, bool trace) {
     constexpr int METRIC = 0;
-    constexpr bool COMPACT = false;
-    if (ef <= 64) return pick4p<METRIC, COMPACT, 2>(d, trace);
-    if (ef <= 96) return pick4p<METRIC, COMPACT, 3>(d, trace);
-    if (ef <= 128) return pick4p<METRIC, COMPACT, 4>(d, trace);
-    return pick4p<METRIC, COMPACT, 8>(d, trace);
+    constexpr int VIS = 0;
+    if (ef <= 64) return pick4p<METRIC, VIS, 2>(d, trace);
+    if (ef <= 96) return pick4p<METRIC, VIS, 3>(d, trace);
+    if (ef <= 128) return pick4p<METRIC, VIS, 4>(d, trace);
+    return pick4p<METRIC, VIS, 8>(d, trace);
 }
 }  // namespace trav
 }  // namespace pa

@@ -5,45 +5,45 @@
 namespace pa {
 namespace trav {
 namespace {
-template <int METRIC, bool COMPACT, int SMAX>
+template <int METRIC, int VIS, int SMAX>
 void* pick4(int d, bool trace) {
-    if (trace) return (void*)k_traverse<METRIC, COMPACT, SMAX, 0, true, true>;
+    if (trace) return (void*)k_traverse<METRIC, VIS, SMAX, 0, true, true>;
     switch (d) {
-        case 32: return (void*)k_traverse<METRIC, COMPACT, SMAX, 4, false, true>;
-        case 48: return (void*)k_traverse<METRIC, COMPACT, SMAX, 6, false, true>;
-        case 64: return (void*)k_traverse<METRIC, COMPACT, SMAX, 8, false, true>;
-        case 128: return (void*)k_traverse<METRIC, COMPACT, SMAX, 16, false, true>;
-        default: return (void*)k_traverse<METRIC, COMPACT, SMAX, 0, false, true>;
+        case 32: return (void*)k_traverse<METRIC, VIS, SMAX, 4, false, true>;
+        case 48: return (void*)k_traverse<METRIC, VIS, SMAX, 6, false, true>;
+        case 64: return (void*)k_traverse<METRIC, VIS, SMAX, 8, false, true>;
+        case 128: return (void*)k_traverse<METRIC, VIS, SMAX, 16, false, true>;
+        default: return (void*)k_traverse<METRIC, VIS, SMAX, 0, false, true>;
     }
 }
-template <int METRIC, bool COMPACT, int SMAX>
+template <int METRIC, int VIS, int SMAX>
 void* pick4p(int d, bool trace) {
-    if (trace) return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 0, true, true>;
+    if (trace) return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 0, true, true>;
     switch (d) {
-        case 32: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 4, false, true>;
-        case 48: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 6, false, true>;
-        case 64: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 8, false, true>;
-        case 128: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 16, false, true>;
-        default: return (void*)k_traverse_pipe<METRIC, COMPACT, SMAX, 0, false, true>;
+        case 32: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 4, false, true>;
+        case 48: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 6, false, true>;
+        case 64: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 8, false, true>;
+        case 128: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 16, false, true>;
+        default: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 0, false, true>;
     }
 }
 }  // namespace
 
 void* traverse_pick_0wh(int ef, int d, bool trace) {
     constexpr int METRIC = 0;
-    constexpr bool COMPACT = false;
-    if (ef <= 64) return pick4<METRIC, COMPACT, 2>(d, trace);
-    if (ef <= 96) return pick4<METRIC, COMPACT, 3>(d, trace);
-    if (ef <= 128) return pick4<METRIC, COMPACT, 4>(d, trace);
-    return pick4<METRIC, COMPACT, 8>(d, trace);
+    constexpr int VIS = 0;
+    if (ef <= 64) return pick4<METRIC, VIS, 2>(d, trace);
+    if (ef <= 96) return pick4<METRIC, VIS, 3>(d, trace);
+    if (ef <= 128) return pick4<METRIC, VIS, 4>(d, trace);
+    return pick4<METRIC, VIS, 8>(d, trace);
 }
 void* traverse_pick_pipe_0wh(int ef, int d, bool trace) {
     constexpr int METRIC = 0;
-    constexpr bool COMPACT = false;
-    if (ef <= 64) return pick4p<METRIC, COMPACT, 2>(d, trace);
-    if (ef <= 96) return pick4p<METRIC, COMPACT, 3>(d, trace);
-    if (ef <= 128) return pick4p<METRIC, COMPACT, 4>(d, trace);
-    return pick4p<METRIC, COMPACT, 8>(d, trace);
+    constexpr int VIS = 0;
+    if (ef <= 64) return pick4p<METRIC, VIS, 2>(d, trace);
+    if (ef <= 96) return pick4p<METRIC, VIS, 3>(d, trace);
+    if (ef <= 128) return pick4p<METRIC, VIS, 4>(d, trace);
+    return pick4p<METRIC, VIS, 8>(d, trace);
 }
 }  // namespace trav
 }  // namespace pa

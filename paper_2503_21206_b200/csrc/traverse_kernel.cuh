@@ -36,6 +36,11 @@ constexpr int kTW = 4;                 // warps per block
 #endif
 constexpr int kIterCap = 1000000;      // Q16 safety cap (status 2)
 
+// Bloom segment hash multipliers (odd; oracle O13 uses the same definition).
+__device__ __forceinline__ constexpr uint32_t bloom_mult(int j) {
+    return j == 0 ? 0x9E3779B1u : (j == 1 ? 0x85EBCA77u : 0xC2B2AE3Du);
+}
+
 __device__ __forceinline__ uint32_t hash1(int32_t v) { return (uint32_t)v * 0x9E3779B1u; }
 __device__ __forceinline__ uint32_t hash2(int32_t v) { return ((uint32_t)v ^ 0x5bd1e995u) * 0x85EBCA77u; }
 
@@ -58,11 +63,11 @@ struct Visited {
 __device__ __forceinline__ uint32_t perm24(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) & 0xFFFFFFu; }
 
 // Returns true iff v was not yet visited (and is now).  `open1` is warp-uniform.
-template <bool COMPACT>
+template <int VIS>
 __device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& in_l2, uint32_t& slot) {
     in_l2 = false;
     const uint32_t S = 1u << vs.log2S;
-    if constexpr (COMPACT) {
+    if constexpr (VIS == 1) {
         volatile uint16_t* H16 = reinterpret_cast<volatile uint16_t*>(vs.H);
         const uint32_t P = perm24(v);
         const uint32_t home = P >> (24 - vs.log2S);
@@ -106,88 +111,16 @@ __device__ __forceinline__ bool visit(Visited& vs, int32_t v, bool open1, bool& 
     return false;   // unreachable while count2 ≤ gmask/2 (guarded by the caller)
 }
 
-// Warp-synchronous variant of visit() without shared-memory atomics (16-bit
-// atomicCAS is emulated with a 32-bit CAS loop): every pending lane probes its
-// window read-only; among lanes that picked the same empty slot the lowest one
-// writes, the others re-probe in the next round (a batch's ids are distinct, so
-// only slot collisions arbitrate).  Same table contents and results as visit().
-template <bool COMPACT>
-__device__ __forceinline__ bool visit_warp(Visited& vs, int32_t v, bool open1, bool& in_l2, uint32_t& slot,
-                                           int lane) {
-    in_l2 = false;
-    const uint32_t S = 1u << vs.log2S;
-    bool pending = v >= 0, isnew = false, to_l2 = false;
-    uint32_t P = 0, home = 0, rem = 0;
-    if (COMPACT && pending) {
-        P = perm24(v);
-        home = P >> (24 - vs.log2S);
-        rem = P & ((1u << (24 - vs.log2S)) - 1u);
-    }
-    while (__ballot_sync(kFull, pending)) {
-        int e = -1;
-        uint32_t val = 0;
-        if (pending) {
-            if constexpr (COMPACT) {
-                const volatile uint16_t* H16 = reinterpret_cast<const volatile uint16_t*>(vs.H);
-                bool done = false;
-                for (uint32_t d = 0; d < 7 && !done; ++d) {
-                    const uint32_t h = (home + d) & (S - 1);
-                    const uint16_t want = (uint16_t)((rem << 3) | d);
-                    const uint16_t cur = H16[h];
-                    if (cur == want) { pending = false; done = true; }                 // visited
-                    else if (cur == 0xFFFFu) {
-                        if (open1) { e = (int)h; val = want; }
-                        else { to_l2 = true; pending = false; }
-                        done = true;
-                    }
-                }
-                if (!done) { to_l2 = true; pending = false; }                          // window full
-            } else {
-                uint32_t h = hash1(v) >> (32 - vs.log2S);
-                for (uint32_t p = 0; p < S; ++p) {
-                    const int32_t cur = vs.H[h];
-                    if (cur == v) { pending = false; break; }
-                    if (cur == -1) {
-                        if (open1) { e = (int)h; val = (uint32_t)v; }
-                        else { to_l2 = true; pending = false; }
-                        break;
-                    }
-                    h = (h + 1) & (S - 1);
-                }
-            }
-        }
-        const unsigned peers = __match_any_sync(kFull, e);
-        if (e >= 0 && (peers & ((1u << lane) - 1u)) == 0) {
-            if constexpr (COMPACT) reinterpret_cast<volatile uint16_t*>(vs.H)[e] = (uint16_t)val;
-            else vs.H[e] = (int32_t)val;
-            pending = false;
-            isnew = true;
-        }
-        __syncwarp();
-    }
-    if (to_l2) {
-        const uint32_t tag = (uint32_t)v + 1u;
-        uint32_t g = hash2(v) & vs.gmask;
-        for (uint32_t p = 0; p <= vs.gmask; ++p) {
-            const uint32_t old = atomicCAS(&vs.G[g], 0u, tag);
-            if (old == 0u) { in_l2 = true; slot = g; isnew = true; break; }
-            if (old == tag) break;
-            g = (g + 1) & vs.gmask;
-        }
-    }
-    return isnew;
-}
-
 // Bulk prefetch of one reduced-vector row into L2 (sm_90+ cp.async.bulk.prefetch).
 __device__ __forceinline__ void prefetch_row_l2(const void* p, int bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
 }
 
 // Lookup-only probe of the level-1 hash (speculation; false negatives only cost a prefetch).
-template <bool COMPACT>
+template <int VIS>
 __device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
     const uint32_t S = 1u << vs.log2S;
-    if constexpr (COMPACT) {
+    if constexpr (VIS == 1) {
         const volatile uint16_t* H16 = reinterpret_cast<const volatile uint16_t*>(vs.H);
         const uint32_t P = perm24(v);
         const uint32_t home = P >> (24 - vs.log2S);
@@ -209,7 +142,7 @@ __device__ __forceinline__ bool visited_l1(const Visited& vs, int32_t v) {
     return false;
 }
 
-template <int METRIC, bool COMPACT, int SMAX, int DPS4, bool TRACE, bool H16>
+template <int METRIC, int VIS, int SMAX, int DPS4, bool TRACE, bool H16>
 __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix, SearchArgs a) {
     const int ELLW = ix.ell_w, NCH = ix.ell_w >> 5;         // ELL row width 32 or 64
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -217,7 +150,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
     const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
     const int efp = (ef + 1) & ~1;                      // keep qs 16-B aligned
     const int qlen = ix.qlen;                           // ≥ dps (fp32 rows) / ≥ rdim_h (fp16 rows)
-    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 + (size_t)S * (COMPACT ? 2 : 4);
+    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 + (size_t)S * (VIS == 1 ? 2 : 4);
     unsigned char* base = smem_raw + per_warp * w;
     uint64_t* C = reinterpret_cast<uint64_t*>(base);
     float* qs = reinterpret_cast<float*>(C + efp);
@@ -242,7 +175,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
         vs.count2 = 0;
         for (int i = lane; i < qlen; i += 32) qs[i] = i < dps ? a.qp[q * dps + i] : 0.f;
         int4* H4 = reinterpret_cast<int4*>(H);
-        for (int i = lane; i < (S >> (COMPACT ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
+        for (int i = lane; i < (S >> (VIS == 1 ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
         __syncwarp();
 
         int csz = 0, hint = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
@@ -254,7 +187,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
             if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
             bool l2 = false;
             uint32_t slot = 0;
-            const bool isnew = visit_warp<COMPACT>(vs, v, open1, l2, slot, lane);
+            const bool isnew = v >= 0 && visit<VIS>(vs, v, open1, l2, slot);
             const unsigned bal = __ballot_sync(kFull, isnew);
             const unsigned bl2 = __ballot_sync(kFull, l2);
             const int nnew = __popc(bal);
@@ -363,7 +296,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
 #pragma unroll
                         for (int c2 = 0; c2 < 2; ++c2) {
                             const int32_t w2 = sv[c2];
-                            if (w2 >= 0 && !visited_l1<COMPACT>(vs, w2))
+                            if (w2 >= 0 && !visited_l1<VIS>(vs, w2))
                                 prefetch_row_l2(H16 ? (const void*)(reinterpret_cast<const __half*>(ix.reduced_h) +
                                                                      (int64_t)w2 * ix.rdim_h)
                                                     : (const void*)(ix.reduced + (int64_t)w2 * dps),
@@ -426,14 +359,16 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
 //      worst, so both are in the ef-truncated list; it is marked checked (in C,
 //      or on the pending key before it is merged) and its row is fetched.
 // The expansion and visit sequences are identical to the sequential kernel.
-template <int METRIC, bool COMPACT, int SMAX, int DPS4, bool TRACE, bool H16>
+template <int METRIC, int VIS, int SMAX, int DPS4, bool TRACE, bool H16>
 __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevIndex ix, SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
     const int efp = (ef + 1) & ~1;
     const int qlen = ix.qlen;
-    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 + (size_t)S * (COMPACT ? 2 : 4);
+    const int bl = a.bloom_log2;                         // VIS == 2: 3 segments × 2^bl bits
+    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 +
+                            (VIS == 2 ? ((size_t)3 << (bl - 3)) : (size_t)S * (VIS == 1 ? 2 : 4));
     unsigned char* base = smem_raw + per_warp * w;
     uint64_t* C = reinterpret_cast<uint64_t*>(base);
     float* qs = reinterpret_cast<float*>(C + efp);
@@ -468,17 +403,63 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
         vs.count2 = 0;
         for (int i = lane; i < qlen; i += 32) qs[i] = i < dps ? a.qp[q * dps + i] : 0.f;
         int4* H4 = reinterpret_cast<int4*>(H);
-        for (int i = lane; i < (S >> (COMPACT ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
+        if constexpr (VIS == 2) {
+            for (int i = lane; i < (3 << (bl - 7)); i += 32) H4[i] = make_int4(0, 0, 0, 0);
+        } else {
+            for (int i = lane; i < (S >> (VIS == 1 ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
+        }
         __syncwarp();
 
         int csz = 0, hint = 0, n_exp = 0, n_dist = 0, n_spill = 0, status = 0;
 
-        auto visit_batch = [&](int32_t v) -> bool {
+        // Visited test-and-insert of one batch of ≤ 32 ids in stored order (lane
+        // order; −1 = none); returns whether this lane's id is new (Alg 1 l.6-7).
+        // `entries`: a5 inserts unconditionally (entries are distinct).
+        auto visit_batch = [&](int32_t v, bool entries) -> bool {
+            if constexpr (VIS == 2) {
+                // Partitioned bloom filter (oracle O13): segment j holds
+                // bit ((uint32)v·A_j) >> (32 − bl).  Sequential test-then-set in lane
+                // order is reproduced exactly: lane b sees the filter plus the bits
+                // of every valid lower lane (a lower lane that is itself judged
+                // visited only adds bits already present), and per-segment hashing
+                // means only equal positions within a segment can coincide, which
+                // one match.any per segment detects.
+                uint32_t* F = reinterpret_cast<uint32_t*>(H);
+                const bool valid = v >= 0;
+                const unsigned lower = __ballot_sync(kFull, valid) & lt_mask;
+                bool covered = !entries;
+                uint32_t wi[3], bm[3];
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const uint32_t p = valid ? (((uint32_t)v * bloom_mult(j)) >> (32 - bl)) : 0xFFFFFFFFu;
+                    wi[j] = ((uint32_t)j << (bl - 5)) + (p >> 5);
+                    bm[j] = 1u << (p & 31);
+                    if (!entries) {
+                        const unsigned peers = __match_any_sync(kFull, p);
+                        const bool c = (peers & lower) != 0 || (valid && (F[wi[j]] & bm[j]) != 0);
+                        covered = covered && c;
+                    }
+                }
+                const bool isnew = valid && !covered;
+                __syncwarp();
+                if (isnew) {
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) atomicOr(&F[wi[j]], bm[j]);
+                }
+                __syncwarp();
+                const unsigned bal = __ballot_sync(kFull, isnew);
+                if (TRACE && isnew) {
+                    const int pos = n_dist + __popc(bal & lt_mask);
+                    if (pos < a.trace_cap) a.trace_visit[q * a.trace_cap + pos] = v;
+                }
+                n_dist += __popc(bal);
+                return isnew;
+            }
             const bool open1 = vs.count1 + 32 <= cap1;
             if (!open1 && vs.count2 + 32 > cap2) { status = 1; return false; }
             bool l2 = false;
             uint32_t slot = 0;
-            const bool isnew = visit_warp<COMPACT>(vs, v, open1, l2, slot, lane);
+            const bool isnew = v >= 0 && visit<VIS>(vs, v, open1, l2, slot);
             const unsigned bal = __ballot_sync(kFull, isnew);
             const unsigned bl2 = __ballot_sync(kFull, l2);
             const int nnew = __popc(bal);
@@ -503,7 +484,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
         for (int j0 = 0; j0 < a.E && status == 0; j0 += 32) {
             const int j = j0 + lane;
             const int32_t v = j < a.E ? a.entries[q * a.E + j] : -1;
-            const bool isnew = visit_batch(v);
+            const bool isnew = visit_batch(v, true);
             if (status != 0) break;
             const uint64_t key = isnew ? make_key(dist(v), v) : kKeyInf;
             const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
@@ -532,7 +513,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
                     if (TRACE && lane == 0 && n_exp < a.trace_cap) a.trace_expand[q * a.trace_cap + n_exp] = u;
                     ++n_exp;
                     // 1. visit u's neighbours, prefetch the new rows into L2
-                    const bool isnew = visit_batch(vv);
+                    const bool isnew = visit_batch(vv, false);
                     if (status != 0) break;
                     if (isnew) prefetch_row_l2(row_ptr(vv), row_bytes);
                     // 2. merge the previous expansion's keys; runner-up r; its row speculatively

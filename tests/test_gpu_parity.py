@@ -48,7 +48,8 @@ def _both(inst, k, ef, trace_cap=4096, **opts):
     ix = pa.Index.from_instance(inst)
     g = run_gpu(ix, inst, k, ef, trace_cap=trace_cap, **opts)
     flags = opts.get("flags", 0)
-    r = orc.search(inst, k=k, ef=ef, stages=1, trace_cap=trace_cap, flags=flags,
+    bl = opts.get("bloom_log2") or None
+    r = orc.search(inst, k=k, ef=ef, stages=1, trace_cap=trace_cap, flags=flags, bloom_log2=bl,
                    **{kk: v for kk, v in opts.items() if kk in ("entries", "ef1") and v})
     ix.close()
     return g, r
@@ -283,3 +284,66 @@ def test_fes_selection_variants_agree(cfg_name, request, monkeypatch):
     ix.close()
     for a, b in zip(outs[:4], outs[4:]):
         assert np.array_equal(a, b)
+
+
+# ------------------------------------------------ NEXT-f1: bloom visited set --
+# The paper's shared-memory bloom filter vs the oracle's O13 mode on
+# the same filter definition: false positives are part of the method, so the
+# trajectories (including which fresh nodes are skipped) must agree exactly.
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("bl", [7, 10])
+def test_bloom_integer_fixture_bit_exact(metric, bl):
+    inst = integer_instance(seed=11, metric=metric, n=500)
+    for ef in (8, 48):
+        g, r = _both(inst, 5, ef, bloom_log2=bl)
+        rep = compare(inst, g, r, 5, ef)
+        assert not rep.fail and rep.tie == 0, (rep, rep.fail[:3])
+        assert np.array_equal(g["trace_visit"], r["trace_visit"]) and np.array_equal(g["trace_expand"], r["trace_expand"])
+        assert np.array_equal(g["ids"], r["ids"]) and np.array_equal(g["d"].astype(np.float64), r["d"])
+        assert np.array_equal(g["n_dist1"], r["n_dist1"])
+
+
+@pytest.mark.parametrize("cfg_name", ["C0", "S1", "S2"])
+@pytest.mark.parametrize("bl", [8, 12])
+def test_bloom_config_parity(cfg_name, bl, request):
+    inst = request.getfixturevalue(cfg_name.lower())
+    cfg = inst["cfg"]
+    g, r = _both(inst, cfg.k, cfg.ef, trace_cap=8192, bloom_log2=bl)
+    rep = compare(inst, g, r, cfg.k, cfg.ef, gt_ids=inst["gt_sub_ids"][:, :cfg.k])
+    print(cfg_name, "bloom", bl, rep, rep.recall_gpu, rep.recall_orc)
+    assert not rep.fail, rep.fail[:5]
+    assert rep.exact >= 0.9 * cfg.m, rep
+    assert np.all(g["status"] == 0)
+
+
+def test_bloom_fp16_integer_fixture_bit_exact():
+    inst = integer_instance(seed=12, n=400)
+    ix = pa.Index.from_instance(inst, reduced_fp16=True)
+    g = run_gpu(ix, inst, 5, 32, trace_cap=4096, bloom_log2=8)
+    ix.close()
+    r = orc.search(rounded16(inst), k=5, ef=32, stages=1, trace_cap=4096, bloom_log2=8)
+    rep = compare(rounded16(inst), g, r, 5, 32)
+    assert not rep.fail and rep.tie == 0, (rep, rep.fail[:3])
+    assert np.array_equal(g["ids"], r["ids"])
+
+
+def test_bloom_full_pipeline(s1):
+    """Stages ②③ keep exact visited sets, so skipped nodes are re-visited
+    (P:L394-395): full-space recall within 0.002 of the oracle's bloom pipeline."""
+    cfg = s1["cfg"]
+    ix = pa.Index.from_instance(s1)
+    ix.attach_host(s1["full_offsets"], s1["full_neighbors"], s1["rotated"])
+    ids, d = ix.search(s1["queries"], k=cfg.k, ef=cfg.ef, stages=pa.PA_STAGES_FULL, bloom_log2=9)
+    ix.close()
+    r = orc.search(s1, k=cfg.k, ef=cfg.ef, stages=3, bloom_log2=9)
+    gt = s1["gt_ids"][:, :cfg.k]
+    assert abs(orc.recall(ids, gt, cfg.k) - orc.recall(r["ids"], gt, cfg.k)) <= 0.002 + 1e-12
+
+
+def test_bloom_rejects_bad_sizes(s1):
+    ix = pa.Index.from_instance(s1)
+    for bl in (3, 17):
+        with pytest.raises(pa.PAError) as e:
+            run_gpu(ix, s1, 10, 64, bloom_log2=bl)
+        assert e.value.status == pa.PA_EINVAL
+    ix.close()
