@@ -566,6 +566,155 @@ __global__ void __launch_bounds__(128) k_fes_select2(FesParams p, int64_t m) {
     }
 }
 
+// Same two-pass selection, latency-restructured (one warp per query):
+//   * the routed cell is found lane-parallel (one ballot over qoff per 32 cells),
+//   * pass 1 reads the row as float4 with NV loads in flight per lane and keeps
+//     per-lane KP smallest 32-bit distance words only (ids are not needed to bound
+//     the E-th smallest distance),
+//   * pass 2 re-reads the row (L2), counts the words ≤ T per lane, places them by a
+//     warp prefix sum and loads the pool ids of the selected entries only,
+//   * ≤ 128 candidates are sorted in registers; larger sets take the smem sort,
+//     more than kSelCap (heavy ties) the rank-merge fallback.
+// Keys and hence entries are identical to k_fes_select / k_fes_select2.
+template <int KPMAX, int SMAX, int NV>
+__global__ void __launch_bounds__(128) k_fes_select3(FesParams p, int64_t m) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int E = p.E, KP = (E + 31) / 32;
+    uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)w * kSelCap;
+    const int64_t nwarps = (int64_t)gridDim.x * 4;
+    for (int64_t pos = (int64_t)blockIdx.x * 4 + w; pos < m; pos += nwarps) {
+        int c = 0;                                        // #cells cc in [1, r) starting at or before pos
+        for (int c0 = 1; c0 < p.r; c0 += 32) {
+            const int cc = c0 + lane;
+            c += __popc(__ballot_sync(kFull, cc < p.r && __ldg(p.qoff + cc) <= pos));
+        }
+        const int pb = __ldg(p.cell_off + c), nc = __ldg(p.cell_off + c + 1) - pb;
+        const float4* srow4 = reinterpret_cast<const float4*>(p.scores + pos * p.sstride);
+        const int32_t* prow = p.pool_ids + pb;
+        const int32_t q = __ldg(p.perm + pos);
+        const int n4 = (nc + 3) >> 2;
+        // ---- pass 1: per-lane KP smallest distance words
+        uint32_t t[KPMAX];
+#pragma unroll
+        for (int i = 0; i < KPMAX; ++i) t[i] = 0xffffffffu;
+        for (int i0 = 0; i0 < n4; i0 += 32 * NV) {
+            float4 v[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int i4 = i0 + u * 32 + lane;
+                v[u] = i4 < n4 ? srow4[i4] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int e0 = (i0 + u * 32 + lane) * 4;
+                const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (e0 + k >= nc) continue;
+                    uint32_t x = ord_of(f[k]);
+                    if (x < t[KP - 1]) {
+#pragma unroll
+                        for (int i = 0; i < KPMAX; ++i)
+                            if (i < KP && x < t[i]) { const uint32_t y = t[i]; t[i] = x; x = y; }
+                    }
+                }
+            }
+        }
+        uint32_t T = 0xffffffffu;
+        if (nc > E) {
+            uint32_t lo = 0;                              // largest T with count(< T) < E (see k_fes_select2)
+            for (int b = 31; b >= 0; --b) {
+                const uint32_t trial = lo | (1u << b);
+                int cnt = 0;
+#pragma unroll
+                for (int i = 0; i < KPMAX; ++i) cnt += (i < KP && t[i] < trial) ? 1 : 0;
+                cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
+                if (cnt < E) lo = trial;
+            }
+            T = lo;
+        }
+        // ---- pass 2: compact every key with distance word ≤ T
+        int M = 0;
+        bool overflow = false;
+        for (int i0 = 0; i0 < n4 && !overflow; i0 += 32 * NV) {
+            float4 v[NV];
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int i4 = i0 + u * 32 + lane;
+                v[u] = i4 < n4 ? srow4[i4] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            uint32_t sel = 0;                             // bit u*4+k: element selected
+            int cnt = 0;
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int e0 = (i0 + u * 32 + lane) * 4;
+                const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool in = e0 + k < nc && ord_of(f[k]) <= T;
+                    sel |= in ? (1u << (u * 4 + k)) : 0u;
+                    cnt += in ? 1 : 0;
+                }
+            }
+            int incl = cnt;                               // warp inclusive prefix sum of the counts
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(kFull, incl, 31);
+            if (M + total > kSelCap) { overflow = true; break; }
+            int at = M + incl - cnt;
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+                const int e0 = (i0 + u * 32 + lane) * 4;
+                const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (sel & (1u << (u * 4 + k))) buf[at++] = make_key(f[k], __ldg(prow + e0 + k));
+            }
+            M += total;
+        }
+        __syncwarp();
+        if (!overflow && M <= 128) {
+            uint64_t t4[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) t4[a] = a * 32 + lane < M ? buf[a * 32 + lane] : kKeyInf;
+            warp_bitonic_regs<4>(t4, lane);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int j = a * 32 + lane;
+                if (j < E) p.entries[(int64_t)q * E + j] = j < M ? key_id(t4[a]) : -1;
+            }
+            for (int j = 128 + lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = -1;
+        } else if (!overflow) {
+            int n2 = 32;
+            while (n2 < M) n2 <<= 1;
+            for (int i = M + lane; i < n2; i += 32) buf[i] = kKeyInf;
+            __syncwarp();
+            warp_bitonic_smem(buf, n2, lane);
+            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < M ? key_id(buf[j]) : -1;
+        } else {                                          // heavy ties: threshold + rank merge
+            uint64_t* C = buf;
+            int csz = 0;
+            const float* srow = p.scores + pos * p.sstride;
+            for (int j0 = 0; j0 < nc; j0 += 32) {
+                const int j = j0 + lane;
+                const uint64_t key = j < nc ? make_key(srow[j], __ldg(prow + j)) : kKeyInf;
+                const uint64_t thresh = csz == E ? C[E - 1] : kKeyInf;
+                const bool pass = key < thresh;
+                const unsigned pbal = __ballot_sync(kFull, pass);
+                if (pbal == 0) continue;
+                int minr;
+                csz = rank_merge<SMAX>(C, csz, E, key, pass, pbal, lane, minr);
+            }
+            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < csz ? key_id(C[j]) : -1;
+        }
+        __syncwarp();
+    }
+}
+
 size_t fes_scores_smem(int kch) { return (size_t)kch * 2 * 16384 + 2 * 16384 + 16; }
 
 }  // namespace
@@ -608,6 +757,10 @@ int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
     if (se && !std::strcmp(se, "merge")) {
         sel = a.E <= 64 ? (void*)k_fes_select<2> : a.E <= 128 ? (void*)k_fes_select<4> : (void*)k_fes_select<8>;
         ssm = (size_t)4 * a.E * 8;
+    } else if (!(se && !std::strcmp(se, "two-pass"))) {
+        sel = a.E <= 64 ? (void*)k_fes_select3<2, 2, 8> : a.E <= 96 ? (void*)k_fes_select3<3, 4, 8>
+            : a.E <= 128 ? (void*)k_fes_select3<4, 4, 8> : (void*)k_fes_select3<8, 8, 8>;
+        ssm = (size_t)4 * kSelCap * 8;
     } else {
         sel = a.E <= 64 ? (void*)k_fes_select2<2, 2> : a.E <= 96 ? (void*)k_fes_select2<3, 4>
             : a.E <= 128 ? (void*)k_fes_select2<4, 4> : (void*)k_fes_select2<8, 8>;

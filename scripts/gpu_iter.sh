@@ -1,5 +1,5 @@
 # Iteration check: GPU tests (optionally a subset), default bench with the NEXT-f1 variants, and
-# extra bench lines given as BENCH_EXTRA="args1;args2".
+# extra bench lines given as BENCH_EXTRA="ENV=1 ENV2=2|args1;|args2".
 mkdir -p gpurun_out; rm -rf /tmp/pa_cache
 TAG=${1:-it}
 python __graft_entry__.py > gpurun_out/build.log 2>&1
@@ -13,7 +13,8 @@ i=0
 for a in "${EX[@]}"; do
   i=$((i+1))
   [ -z "$a" ] && continue
-  eval "$a timeout 900 python bench.py --steps 5 --warmup 3 --no-full --no-cpu-baseline --variants= --cache /tmp/pa_cache" > gpurun_out/bench_${TAG}_x$i.json 2> gpurun_out/bench_${TAG}_x$i.log
+  envs="${a%%|*}"; args="${a#*|}"; [ "$envs" = "$a" ] && envs=""
+  eval "env $envs timeout 900 python bench.py --steps 5 --warmup 3 --no-full --no-cpu-baseline --variants= --cache /tmp/pa_cache $args" > gpurun_out/bench_${TAG}_x$i.json 2> gpurun_out/bench_${TAG}_x$i.log
   python -c "import json;d=json.load(open('gpurun_out/bench_${TAG}_x$i.json'));print('x$i', '$a', d['value'], d['roofline']['traverse_ms'], d['roofline']['frac'], d['config']['ef'], d['config']['recall_at_10_gt_sub'])"
 done
 if [ -n "$MINB_EXTRA" ]; then
@@ -23,4 +24,12 @@ if [ -n "$MINB_EXTRA" ]; then
     python -c "import json;d=json.load(open('gpurun_out/bench_${TAG}_minb.json'));print('minb $MINB_EXTRA', '$a', d['value'], d['roofline']['traverse_ms'], d['roofline']['frac'], d['config']['ef'], d['config']['recall_at_10_gt_sub'])"
   done
   python paper_2503_21206_b200/build.py --force > /dev/null 2>&1
+fi
+if [ -n "$NCU" ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_(project|fes|traverse|bucket)" --csv \
+     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-full --no-cpu-baseline --variants= --cache /tmp/pa_cache > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$NCU" -s 4 -c 1 \
+     -o gpurun_out/prof_$TAG -f python bench.py --steps 1 --warmup 3 --ef 96 --no-full --no-cpu-baseline --variants= --cache /tmp/pa_cache > gpurun_out/ncu_full_$TAG.log 2>&1
+  python scripts/ncu_summary.py gpurun_out/prof_$TAG.ncu-rep gpurun_out/launches_$TAG.csv > gpurun_out/prof_$TAG.md 2>&1
+  grep -E "Duration|dram__bytes|stall samples|Achieved Occ|Registers" gpurun_out/prof_$TAG.md; tail -8 gpurun_out/prof_$TAG.md
 fi

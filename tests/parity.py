@@ -133,14 +133,18 @@ def compare(inst, gpu: dict, ref: dict, k: int, ef: int, gt_ids=None, check_trac
                 continue
             rep.fail.append((q, "identical expansions but different visits"))
             continue
-        # common prefix of t expansions: visits so far are identical?
-        # visits produced by the first t expansions = entries + rows of xo[:t]
+        # common prefix of t expansions: are the visits so far identical?  The
+        # oracle's visit trace fixes which neighbours of the common expansions
+        # were new (rows hold distinct ids and a visited — or bloom-positive —
+        # id never becomes new again), so the prefix is found by matching each
+        # row, in stored order, against the trace; this holds for the exact
+        # visited set and for the bloom filter (O13) alike.
+        off, nb = inst["sub_offsets"], inst["sub_neighbors"]
         vis_set = set(vo[:nE].tolist())
         nvis_prefix = nE
         for u in xo[:t]:
-            off, nb = inst["sub_offsets"], inst["sub_neighbors"]
             for v in nb[off[u]:off[u + 1]]:
-                if v not in vis_set:
+                if nvis_prefix < nv_o and vo[nvis_prefix] == v:
                     vis_set.add(int(v))
                     nvis_prefix += 1
         if not np.array_equal(vg[nE:nvis_prefix], vo[nE:nvis_prefix]):

@@ -271,19 +271,23 @@ def test_fp16_storage_full_pipeline(s1):
 
 @pytest.mark.parametrize("cfg_name", ["S1", "S2", "C0"])
 def test_fes_selection_variants_agree(cfg_name, request, monkeypatch):
-    """The two-pass (threshold + single sort) FES selection returns exactly the
-    entries of the rank-merge selection (same GEMM scores, same keys)."""
+    """The latency-restructured selection (default), the two-pass (threshold +
+    single sort) selection and the rank-merge selection return exactly the same
+    entries (same GEMM scores, same keys)."""
     inst = request.getfixturevalue(cfg_name.lower())
     cfg = inst["cfg"]
     ix = pa.Index.from_instance(inst)
     outs = []
-    for sel in ("two-pass", "merge"):
-        monkeypatch.setenv("PA_FES_SELECT", sel)
-        for ef in (10, 64, 96, 256):
-            outs.append(run_gpu(ix, inst, cfg.k, ef)["entries"])
+    for sel in ("default", "two-pass", "merge"):
+        if sel == "default":
+            monkeypatch.delenv("PA_FES_SELECT", raising=False)
+        else:
+            monkeypatch.setenv("PA_FES_SELECT", sel)
+        outs.append([run_gpu(ix, inst, cfg.k, ef)["entries"] for ef in (10, 64, 96, 256)])
     ix.close()
-    for a, b in zip(outs[:4], outs[4:]):
-        assert np.array_equal(a, b)
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert np.array_equal(a, b)
 
 
 # ------------------------------------------------ NEXT-f1: bloom visited set --
