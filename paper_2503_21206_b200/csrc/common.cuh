@@ -149,62 +149,6 @@ __device__ __forceinline__ int rank_merge(uint64_t* C, int csz, int cap, uint64_
     return min(csz + np, cap);
 }
 
-// Same contract as rank_merge, fewer instructions per passing key: each passing
-// lane finds its key's rank in C by a branch-free binary search over the sorted
-// smem list (log2(32·SMAX) probes, all passing lanes at once); the broadcast loop
-// only accumulates the right shift of C's entries and the key's rank among the
-// passing keys (no ballots).  Keys are unique, so positions are as in rank_merge.
-template <int SMAX>
-__device__ __forceinline__ int rank_merge_bs(uint64_t* C, int csz, int cap, uint64_t key, bool pass, unsigned pb,
-                                             int lane, int& minr) {
-    uint64_t c[SMAX];
-    int sh[SMAX];
-#pragma unroll
-    for (int t = 0; t < SMAX; ++t) {
-        const int i = lane + 32 * t;
-        c[t] = i < csz ? C[i] : kKeyInf;
-        sh[t] = 0;
-    }
-    const int np = __popc(pb);
-    int rc = 0;                                       // #C entries < key
-    if (pass) {
-#pragma unroll
-        for (int step = 32 * SMAX >= 256 ? 256 : (32 * SMAX >= 128 ? 128 : 64); step > 0; step >>= 1)
-            if (rc + step <= csz && C[rc + step - 1] < key) rc += step;
-    }
-    minr = (int)__reduce_min_sync(kFull, pass ? (unsigned)rc : 0xffffffffu);
-    int rn = 0;                                       // #passing keys < key
-    while (pb) {
-        const int s0 = __ffs(pb) - 1;
-        pb &= pb - 1;
-        const int s1 = pb ? __ffs(pb) - 1 : s0;
-        const bool two = pb != 0;
-        pb = two ? (pb & (pb - 1)) : pb;
-        const uint32_t h0 = __shfl_sync(kFull, (uint32_t)(key >> 32), s0);
-        const uint32_t l0 = __shfl_sync(kFull, (uint32_t)key, s0);
-        const uint32_t h1 = __shfl_sync(kFull, (uint32_t)(key >> 32), s1);
-        const uint32_t l1 = __shfl_sync(kFull, (uint32_t)key, s1);
-        const uint64_t x0 = ((uint64_t)h0 << 32) | l0;
-        const uint64_t x1 = two ? (((uint64_t)h1 << 32) | l1) : kKeyInf;
-#pragma unroll
-        for (int t = 0; t < SMAX; ++t) sh[t] += (c[t] > x0 ? 1 : 0) + (c[t] > x1 ? 1 : 0);
-        rn += (x0 < key ? 1 : 0) + (x1 < key ? 1 : 0);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < SMAX; ++t) {
-        const int i = lane + 32 * t;
-        const int pos = i + sh[t];
-        if (i < csz && pos < cap) C[pos] = c[t];
-    }
-    if (pass) {
-        const int pos = rc + rn;
-        if (pos < cap) C[pos] = key;
-    }
-    __syncwarp();
-    return min(csz + np, cap);
-}
-
 // Direct-form distance (Alg 1 l.8) between an smem query row and a global row
 // of `dps` floats (multiple of 4, 16-B aligned): L2 = Σ(x−q)², IP = −Σ x·q.
 // Four independent fp32 FMA chains over float4 slices (Q24: fp32, RNE, FMA).
@@ -251,9 +195,19 @@ __device__ __forceinline__ void fma2(float ax, float ay, float bx, float by, flo
 }
 // acc[0..3] += (v − w)² (L2) or v·w (IP), component-wise: the same four fp32
 // chains as the scalar code, issued as two packed pairs.
-template <int METRIC>
+// PACKED selects the fp32x2 form: measured on C1 it is 9% slower in the fp32-row
+// traversal (register pressure at the 80-register budget) and 1% faster with
+// binary16 rows, so only the binary16 path uses it.
+template <int METRIC, bool PACKED>
 __device__ __forceinline__ void acc4(const float4 v, const float4 w, float& a0, float& a1, float& a2, float& a3) {
-    if (METRIC == 0) {
+    if (!PACKED) {
+        if (METRIC == 0) {
+            const float d0 = v.x - w.x, d1 = v.y - w.y, d2 = v.z - w.z, d3 = v.w - w.w;
+            a0 = fmaf(d0, d0, a0); a1 = fmaf(d1, d1, a1); a2 = fmaf(d2, d2, a2); a3 = fmaf(d3, d3, a3);
+        } else {
+            a0 = fmaf(v.x, w.x, a0); a1 = fmaf(v.y, w.y, a1); a2 = fmaf(v.z, w.z, a2); a3 = fmaf(v.w, w.w, a3);
+        }
+    } else if (METRIC == 0) {
         float d0, d1, d2, d3;
         sub2(v.x, v.y, w.x, w.y, d0, d1);
         sub2(v.z, v.w, w.z, w.w, d2, d3);
@@ -285,7 +239,7 @@ __device__ __forceinline__ float row_dist_t(const float* __restrict__ qs, const 
 #pragma unroll
             for (int i = 0; i < G; ++i) v[i] = __ldg(x4 + g + i);
 #pragma unroll
-            for (int i = 0; i < G; ++i) acc4<METRIC>(v[i], q4[g + i], a0, a1, a2, a3);
+            for (int i = 0; i < G; ++i) acc4<METRIC, false>(v[i], q4[g + i], a0, a1, a2, a3);
         }
         const float s = (a0 + a1) + (a2 + a3);
         return METRIC == 0 ? s : -s;
@@ -300,11 +254,11 @@ __device__ __forceinline__ void acc8(const uint4 u, const float4 w0, const float
     const __half2* h = reinterpret_cast<const __half2*>(&u);
     const float2 f0 = __half22float2(h[0]), f1 = __half22float2(h[1]), f2 = __half22float2(h[2]), f3 = __half22float2(h[3]);
     if (metric == 0) {
-        acc4<0>(make_float4(f0.x, f0.y, f1.x, f1.y), w0, a0, a1, a2, a3);
-        acc4<0>(make_float4(f2.x, f2.y, f3.x, f3.y), w1, a0, a1, a2, a3);
+        acc4<0, true>(make_float4(f0.x, f0.y, f1.x, f1.y), w0, a0, a1, a2, a3);
+        acc4<0, true>(make_float4(f2.x, f2.y, f3.x, f3.y), w1, a0, a1, a2, a3);
     } else {
-        acc4<1>(make_float4(f0.x, f0.y, f1.x, f1.y), w0, a0, a1, a2, a3);
-        acc4<1>(make_float4(f2.x, f2.y, f3.x, f3.y), w1, a0, a1, a2, a3);
+        acc4<1, true>(make_float4(f0.x, f0.y, f1.x, f1.y), w0, a0, a1, a2, a3);
+        acc4<1, true>(make_float4(f2.x, f2.y, f3.x, f3.y), w1, a0, a1, a2, a3);
     }
 }
 

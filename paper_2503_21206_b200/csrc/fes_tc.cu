@@ -580,7 +580,9 @@ template <int KPMAX, int SMAX, int NV>
 __global__ void __launch_bounds__(128) k_fes_select3(FesParams p, int64_t m) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int E = p.E, KP = (E + 31) / 32;
+    // 2·ceil(E/32) words per lane: a lane rarely holds more of the row's E smallest
+    // than that, so T is close to the true E-th smallest word and ≤ 128 keys pass
+    const int E = p.E, KP = min(KPMAX, 2 * ((E + 31) / 32));
     uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)w * kSelCap;
     const int64_t nwarps = (int64_t)gridDim.x * 4;
     for (int64_t pos = (int64_t)blockIdx.x * 4 + w; pos < m; pos += nwarps) {
@@ -758,8 +760,9 @@ int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
         sel = a.E <= 64 ? (void*)k_fes_select<2> : a.E <= 128 ? (void*)k_fes_select<4> : (void*)k_fes_select<8>;
         ssm = (size_t)4 * a.E * 8;
     } else if (!(se && !std::strcmp(se, "two-pass"))) {
-        sel = a.E <= 64 ? (void*)k_fes_select3<2, 2, 8> : a.E <= 96 ? (void*)k_fes_select3<3, 4, 8>
-            : a.E <= 128 ? (void*)k_fes_select3<4, 4, 8> : (void*)k_fes_select3<8, 8, 8>;
+        sel = a.E <= 32 ? (void*)k_fes_select3<2, 2, 8> : a.E <= 64 ? (void*)k_fes_select3<4, 2, 8>
+            : a.E <= 96 ? (void*)k_fes_select3<6, 4, 8> : a.E <= 128 ? (void*)k_fes_select3<8, 4, 8>
+            : (void*)k_fes_select3<16, 8, 8>;
         ssm = (size_t)4 * kSelCap * 8;
     } else {
         sel = a.E <= 64 ? (void*)k_fes_select2<2, 2> : a.E <= 96 ? (void*)k_fes_select2<3, 4>

@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
         auto merge_keys = [&](uint64_t key, bool pass, unsigned pb) {
             if (pb == 0) return;
             int minr;
-            csz = rank_merge_bs<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
+            csz = rank_merge<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
             hint = min(hint, minr);
         };
         // ---- a5: C := entries, visited := entries (sequential merges)
