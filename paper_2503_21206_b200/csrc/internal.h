@@ -14,10 +14,12 @@ struct DevIndex {
     int32_t fes_r = 0;
     int64_t pool_n = 0;
     float* basis = nullptr;                    // [dim][dim] row-major V
-    float* reduced = nullptr;                  // [n][rdim_pad] (non-members: zero rows); null in fp16 mode
-    void* reduced_h = nullptr;                 // [n][rdim_h] binary16 rows (NEXT-f1 storage), rdim_h = round8(d')
+    float* reduced = nullptr;                  // [n][rstride] (first rdim_pad used; non-members: zero rows); null in fp16 mode
+    void* reduced_h = nullptr;                 // [n][rstride_h] binary16 rows (NEXT-f1 storage), first rdim_h = round8(d') used
     int32_t rdim_h = 0;
     int32_t qlen = 0;                          // q' length staged in smem by the traversal (≥ row length)
+    int32_t rstride = 0;                       // row stride of `reduced` in floats: multiple of 32 (128-B lines)
+    int32_t rstride_h = 0;                     // row stride of `reduced_h` in halves: multiple of 64 (128-B lines)
     int32_t* ell = nullptr;                    // [n][ell_w]
     float* centroids = nullptr;                // [r][rdim_pad]
     int32_t* cell_off = nullptr;               // [r+1]

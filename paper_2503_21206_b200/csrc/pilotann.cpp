@@ -471,6 +471,12 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     d.rdim_h = (dp + 7) & ~7;
     d.qlen = p->reduced_fp16 ? std::max(dps, d.rdim_h) : dps;
     const bool f16 = p->reduced_fp16 != 0;
+    // Rows start on 128-B lines and the traversal reads each with 8 lanes × 16 B per
+    // load (whole lines of 4 rows per instruction): the stride is rounded up to 128 B
+    // (e.g. d' = 48 fp32: 192 B of data in a 256-B slot); the padding is never read.
+    d.rstride = (dps + 31) & ~31;
+    d.rstride_h = (d.rdim_h + 63) & ~63;
+    const int rs = f16 ? d.rstride_h : d.rstride;
     auto bail = [&](pa_status s) { pa_destroy(ix); return s; };
     {
         std::lock_guard<std::mutex> g(g_reg_mu);
@@ -491,16 +497,16 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     // reduced vectors [n][dps] fp32 or [n][rdim_h] binary16 (zero rows for non-members), staged in chunks
     if (f16) {
         __half* rh = nullptr;
-        CUB(cudaMalloc((void**)&rh, sizeof(__half) * (size_t)n * d.rdim_h));
+        CUB(cudaMalloc((void**)&rh, sizeof(__half) * (size_t)n * d.rstride_h));
         d.reduced_h = rh;
     } else {
-        CUB(dalloc(&d.reduced, (size_t)n * dps));
+        CUB(dalloc(&d.reduced, (size_t)n * d.rstride));
     }
     CUB(dalloc(&d.ell, (size_t)n * d.ell_w));
     {
         const int64_t chunk = 1 << 20;
-        std::vector<float> rb((size_t)std::min(chunk, n) * dps);
-        std::vector<__half> hb(f16 ? (size_t)std::min(chunk, n) * d.rdim_h : 0);
+        std::vector<float> rb(f16 ? 0 : (size_t)std::min(chunk, n) * rs);
+        std::vector<__half> hb(f16 ? (size_t)std::min(chunk, n) * rs : 0);
         std::vector<int32_t> eb((size_t)std::min(chunk, n) * d.ell_w);
         for (int64_t s0 = 0; s0 < n; s0 += chunk) {
             int64_t s1 = std::min(n, s0 + chunk);
@@ -508,16 +514,16 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
                 for (int64_t i = lo; i < hi; ++i) {
                     int64_t u = s0 + i;
                     if (f16) {
-                        __half* dh = &hb[(size_t)i * d.rdim_h];
-                        for (int j = 0; j < d.rdim_h; ++j)
+                        __half* dh = &hb[(size_t)i * rs];
+                        for (int j = 0; j < rs; ++j)
                             dh[j] = __float2half_rn(member[u] && j < dp ? RED[u * dp + j] : 0.f);
                     } else {
-                        float* dst = &rb[(size_t)i * dps];
+                        float* dst = &rb[(size_t)i * rs];
                         if (member[u]) {
                             std::memcpy(dst, RED + u * dp, sizeof(float) * dp);
-                            for (int j = dp; j < dps; ++j) dst[j] = 0.f;
+                            for (int j = dp; j < rs; ++j) dst[j] = 0.f;
                         } else {
-                            std::memset(dst, 0, sizeof(float) * dps);
+                            std::memset(dst, 0, sizeof(float) * rs);
                         }
                     }
                     int32_t* row = &eb[(size_t)i * d.ell_w];
@@ -526,10 +532,10 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
                 }
             });
             if (f16)
-                CUB(cudaMemcpy(static_cast<__half*>(d.reduced_h) + s0 * d.rdim_h, hb.data(),
-                               sizeof(__half) * (s1 - s0) * d.rdim_h, cudaMemcpyHostToDevice));
+                CUB(cudaMemcpy(static_cast<__half*>(d.reduced_h) + s0 * rs, hb.data(),
+                               sizeof(__half) * (s1 - s0) * rs, cudaMemcpyHostToDevice));
             else
-                CUB(cudaMemcpy(d.reduced + s0 * dps, rb.data(), sizeof(float) * (s1 - s0) * dps, cudaMemcpyHostToDevice));
+                CUB(cudaMemcpy(d.reduced + s0 * rs, rb.data(), sizeof(float) * (s1 - s0) * rs, cudaMemcpyHostToDevice));
             CUB(cudaMemcpy(d.ell + s0 * d.ell_w, eb.data(), sizeof(int32_t) * (s1 - s0) * d.ell_w, cudaMemcpyHostToDevice));
         }
     }

@@ -73,7 +73,7 @@ size_t smem_bytes(const DevIndex& ix, const SearchArgs& a) {
     const size_t efp = (size_t)((a.ef + 1) & ~1);
     const size_t vis = a.bloom_log2 > 0 ? ((size_t)3 << (a.bloom_log2 - 3))
                                         : ((size_t)(use_compact(ix, a) ? 2 : 4) << a.hash_log2);
-    size_t per_warp = efp * 8 + (size_t)ix.qlen * 4 + vis;
+    size_t per_warp = efp * 8 + (size_t)ix.qlen * 4 + 128 + vis;   // + 32 ids of compaction scratch
     return per_warp * kTW;
 }
 }  // namespace

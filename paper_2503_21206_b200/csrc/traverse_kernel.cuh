@@ -210,10 +210,10 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
             if (isnew) {
                 float dv;
                 if constexpr (H16)
-                    dv = row_dist_h<METRIC, DPS4>(qs, reinterpret_cast<const __half*>(ix.reduced_h) + (int64_t)v * ix.rdim_h,
+                    dv = row_dist_h<METRIC, DPS4>(qs, reinterpret_cast<const __half*>(ix.reduced_h) + (int64_t)v * ix.rstride_h,
                                                   ix.rdim_h);
                 else
-                    dv = row_dist_t<METRIC, DPS4>(qs, ix.reduced + (int64_t)v * dps, dps);
+                    dv = row_dist_t<METRIC, DPS4>(qs, ix.reduced + (int64_t)v * ix.rstride, dps);
                 key = make_key(dv, v);
             }
             {
@@ -298,8 +298,8 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
                             const int32_t w2 = sv[c2];
                             if (w2 >= 0 && !visited_l1<VIS>(vs, w2))
                                 prefetch_row_l2(H16 ? (const void*)(reinterpret_cast<const __half*>(ix.reduced_h) +
-                                                                     (int64_t)w2 * ix.rdim_h)
-                                                    : (const void*)(ix.reduced + (int64_t)w2 * dps),
+                                                                     (int64_t)w2 * ix.rstride_h)
+                                                    : (const void*)(ix.reduced + (int64_t)w2 * ix.rstride),
                                                 H16 ? ix.rdim_h * 2 : dps * 4);
                         }
                     }
@@ -367,12 +367,13 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
     const int efp = (ef + 1) & ~1;
     const int qlen = ix.qlen;
     const int bl = a.bloom_log2;                         // VIS == 2: 3 segments × 2^bl bits
-    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 +
+    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 + 128 +
                             (VIS == 2 ? ((size_t)3 << (bl - 3)) : (size_t)S * (VIS == 1 ? 2 : 4));
     unsigned char* base = smem_raw + per_warp * w;
     uint64_t* C = reinterpret_cast<uint64_t*>(base);
     float* qs = reinterpret_cast<float*>(C + efp);
-    int32_t* H = reinterpret_cast<int32_t*>(qs + qlen);
+    int32_t* scr = reinterpret_cast<int32_t*>(qs + qlen);      // 32 compacted new ids
+    int32_t* H = scr + 32;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int64_t gw = (int64_t)blockIdx.x * kTW + w;
 
@@ -384,15 +385,25 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
     vs.gmask = (1u << a.spill_log2) - 1u;
     const int cap1 = S >> 1, cap2 = (int)(vs.gmask >> 1);
 
-    auto row_ptr = [&](int32_t v) -> const void* {
-        if constexpr (H16) return reinterpret_cast<const __half*>(ix.reduced_h) + (int64_t)v * ix.rdim_h;
-        else return ix.reduced + (int64_t)v * dps;
-    };
-    auto dist = [&](int32_t v) -> float {
-        if constexpr (H16) return row_dist_h<METRIC, DPS4>(qs, reinterpret_cast<const __half*>(row_ptr(v)), ix.rdim_h);
-        else return row_dist_t<METRIC, DPS4>(qs, reinterpret_cast<const float*>(row_ptr(v)), dps);
-    };
+    const unsigned char* rows = H16 ? reinterpret_cast<const unsigned char*>(ix.reduced_h)
+                                    : reinterpret_cast<const unsigned char*>(ix.reduced);
+    const int64_t stride = H16 ? (int64_t)ix.rstride_h * 2 : (int64_t)ix.rstride * 4;
+    auto row_ptr = [&](int32_t v) -> const void* { return rows + (int64_t)v * stride; };
     const int row_bytes = H16 ? ix.rdim_h * 2 : dps * 4;
+    const int nvr = row_bytes >> 4;                             // 16-B chunks per row
+    // Keys of this batch's new ids (Alg 1 l.8): compacted, lane r holds the key of
+    // the r-th new id (lane order), lanes ≥ #new hold kKeyInf.
+    auto new_keys = [&](int32_t v, bool isnew) -> uint64_t {
+        const unsigned bal = __ballot_sync(kFull, isnew);
+        const int nnew = __popc(bal);
+        if (nnew == 0) return kKeyInf;
+        if (isnew) scr[__popc(bal & lt_mask)] = v;
+        __syncwarp();
+        const int32_t cid = lane < nnew ? scr[lane] : 0;
+        __syncwarp();
+        const float d = group_dists<METRIC, DPS4, H16>(qs, rows, stride, nvr, cid, nnew, lane);
+        return lane < nnew ? make_key(d, cid) : kKeyInf;
+    };
 
     for (;;) {
         int64_t q = 0;
@@ -486,7 +497,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
             const int32_t v = j < a.E ? a.entries[q * a.E + j] : -1;
             const bool isnew = visit_batch(v, true);
             if (status != 0) break;
-            const uint64_t key = isnew ? make_key(dist(v), v) : kKeyInf;
+            const uint64_t key = new_keys(v, isnew);
             const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
             const bool pass = key < thresh;
             merge_keys(key, pass, __ballot_sync(kFull, pass));
@@ -531,7 +542,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
                         sv = __ldg(ix.ell + (int64_t)spec_u * 32 + lane);
                     }
                     // 3. δ' of the new neighbours, filter against C's worst
-                    const uint64_t key = isnew ? make_key(dist(vv), vv) : kKeyInf;
+                    const uint64_t key = new_keys(vv, isnew);
                     const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
                     bool pass = key < thresh;
                     const unsigned pb = __ballot_sync(kFull, pass);
