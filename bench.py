@@ -302,8 +302,8 @@ def run_ours(args, rank, world, local_rank):
     rec_full = recall_at(out_i.cpu().numpy(), inst["gt_ids"], k)
     qps = m * world / (ms / 1e3)
 
-    # ---- NEXT-f1 variants: binary16-stored reduced rows and/or the paper's bloom
-    # visited set, each at its own smallest ef with Recall@10 (GT_sub) >= 0.90
+    # ---- variants beside the headline: exact visited set and/or binary16-stored
+    # reduced rows (NEXT-f1), each at its own smallest ef with Recall@10 (GT_sub) >= 0.90
     def variant(name, what, fp16, bloom):
         ixv = pa.Index.from_instance(inst, device=local_rank, reduced_fp16=fp16) if fp16 else ix
 
@@ -338,15 +338,14 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_f1:
         want = [x for x in args.variants.split(",") if x]
         specs = {
-            "fp16": ("NEXT-f1: reduced rows stored as binary16 (rounded once at build; fp32 arithmetic; "
-                     "parity vs the oracle on the same rounded values)", True, 0),
-            "bloom": (f"NEXT-f1: the paper's shared-memory bloom visited set (P:L392-395), 3 x 2^{args.bloom_bits} "
-                      "bits per query; parity vs the oracle's O13 mode", False, args.bloom_bits),
-            "bloom_fp16": ("NEXT-f1: bloom visited set + binary16 rows", True, args.bloom_bits),
+            "exact": ("exact visited set (smem hash + global spill) instead of the paper's bloom filter; "
+                      "fp32 rows", False, 0),
+            "fp16": ("NEXT-f1: reduced rows stored as binary16 (rounded once at build; fp32 arithmetic; parity "
+                     f"vs the oracle on the same rounded values), bloom 3 x 2^{args.bloom_bits}", True, args.bloom_bits),
+            "exact_fp16": ("exact visited set + binary16 rows", True, 0),
         }
         for name in want:
-            if name in specs and not (name == "fp16" and args.reduced == "fp16") and \
-                    not (name == "bloom" and args.bloom):
+            if name in specs and args.reduced == "fp32" and not (name == "exact" and not args.bloom):
                 variants[name] = variant(name, *specs[name])
                 log(f"[rank {rank}] variant {name}: {variants[name]['value']:.0f} q/s ef={variants[name]['ef']} "
                     f"trav {variants[name]['traverse_ms']:.3f} ms")
@@ -406,7 +405,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": m * cfg.D * 4,
                     "d2h_bytes_per_step": m * k * 8},
             "end_to_end_full": full,
-            "f1_variants": variants,
+            "variants": variants,
             "gpu_launches": launches,
             "clocks": clocks,
         }
@@ -479,10 +478,11 @@ def main():
     ap.add_argument("--repeat-queries", type=int, default=1, help="experiment only: tile the query batch R times")
     ap.add_argument("--reduced", default="fp32", choices=["fp32", "fp16"],
                     help="storage of the reduced rows on the GPU (fp16 = NEXT-f1; parity on the rounded values)")
-    ap.add_argument("--bloom", type=int, default=0,
-                    help="headline path with the bloom visited set of 3 x 2^BLOOM bits (0 = exact set)")
-    ap.add_argument("--bloom-bits", type=int, default=12, help="bloom size of the bloom variants")
-    ap.add_argument("--variants", default="fp16,bloom,bloom_fp16", help="NEXT-f1 variants measured beside the headline")
+    ap.add_argument("--bloom", type=int, default=12,
+                    help="visited set of the headline path: the paper's shared-memory bloom filter (P:L392-395) "
+                         "of 3 x 2^BLOOM bits per query; 0 = exact set")
+    ap.add_argument("--bloom-bits", type=int, default=12, help="bloom size of the binary16 variant")
+    ap.add_argument("--variants", default="exact,fp16,exact_fp16", help="variants measured beside the headline")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

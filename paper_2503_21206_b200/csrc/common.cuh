@@ -284,62 +284,64 @@ __device__ __forceinline__ float row_dist_h(const float* __restrict__ qs, const 
 }
 
 // δ' of up to 32 new ids (compacted: lane r holds the r-th id in `cid`, r < nnew)
-// with 8 lanes per row: lane j of group g reads 16-B chunks k·8 + j of row 4p + g
-// in pass p, so every load instruction fetches whole 128-B lines of 4 rows (rows
-// start on 128-B lines: `stride` bytes, a multiple of 128).  Measured on this GPU
-// (scripts/micro/gather_bw.cu) random 16-B-per-lane row gathers saturate at
-// ~1.3 TB/s, 128-B-line groups reach 3.6–6 TB/s.  Partial sums are reduced over
-// the 8 lanes (butterfly) and sent back to lane r.  NVR = 16-B chunks per row
-// (fp32: d'/4, binary16: d'/8; 0 = runtime `nvr`).  Returns lane r's δ'.
-template <int METRIC, int NVR, bool H16>
+// with L lanes per row: lane j of group g reads 16-B chunks k·L + j of row
+// RPP·p + g in pass p (RPP = 32/L rows per pass), so each load instruction
+// fetches L·16 contiguous bytes of each of RPP rows (rows start on 128-B lines:
+// `stride` bytes, a multiple of 128).  Measured on this GPU
+// (scripts/micro/gather_bw.cu), random gathers with 16 B per lane per row cap at
+// ~1.3 TB/s; 64-B (L = 4) and 128-B (L = 8) row segments reach 2.5–6 TB/s.  Partial
+// sums are reduced over the L lanes (butterfly) and sent back to lane r.  NVR =
+// 16-B chunks per row (fp32: d'/4, binary16: d'/8; 0 = runtime `nvr`).  Returns
+// lane r's δ'.
+template <int METRIC, int NVR, bool H16, int L>
 __device__ __forceinline__ float group_dists(const float* __restrict__ qs, const unsigned char* __restrict__ base,
                                              int64_t stride, int nvr, int32_t cid, int nnew, int lane) {
-    const int g = lane >> 3, j = lane & 7;
+    constexpr int RPP = 32 / L;
+    const int g = lane / L, j = lane % L;
     const float4* q4 = reinterpret_cast<const float4*>(qs);
-    constexpr int F = NVR > 0 ? (NVR + 7) / 8 : 1;          // chunks per lane (compile-time rows)
-    constexpr int PG = F >= 4 ? 2 : 4;                       // passes whose loads are in flight together
+    constexpr int F = NVR > 0 ? (NVR + L - 1) / L : 1;      // chunks per lane (compile-time rows)
+    constexpr int PG = F >= 4 ? 1 : (F >= 2 ? 2 : 4);       // passes whose loads are in flight together
     float mine = 0.f;
-    for (int p0 = 0; p0 * 4 < nnew; p0 += PG) {
+    for (int p0 = 0; p0 * RPP < nnew; p0 += PG) {
         uint4 v[PG][F];
         int32_t rid[PG];
 #pragma unroll
         for (int pp = 0; pp < PG; ++pp) {
-            const int rr = (p0 + pp) * 4 + g;
+            const int rr = (p0 + pp) * RPP + g;
             rid[pp] = __shfl_sync(kFull, cid, rr & 31);
             if (NVR > 0) {
                 const uint4* row = reinterpret_cast<const uint4*>(base + (int64_t)rid[pp] * stride);
 #pragma unroll
                 for (int k = 0; k < F; ++k)
-                    v[pp][k] = (rr < nnew && k * 8 + j < NVR) ? __ldg(row + k * 8 + j) : make_uint4(0u, 0u, 0u, 0u);
+                    v[pp][k] = (rr < nnew && k * L + j < NVR) ? __ldg(row + k * L + j) : make_uint4(0u, 0u, 0u, 0u);
             }
         }
 #pragma unroll
         for (int pp = 0; pp < PG; ++pp) {
-            if ((p0 + pp) * 4 >= nnew) break;                      // warp-uniform
-            const int rr = (p0 + pp) * 4 + g;
+            if ((p0 + pp) * RPP >= nnew) break;                    // warp-uniform
+            const int rr = (p0 + pp) * RPP + g;
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
             if (NVR > 0) {
 #pragma unroll
                 for (int k = 0; k < F; ++k) {
-                    const int c = k * 8 + j;
+                    const int c = k * L + j;
                     if (c >= NVR) continue;
                     if constexpr (H16) acc8(v[pp][k], q4[2 * c], q4[2 * c + 1], METRIC, a0, a1, a2, a3);
                     else acc4<METRIC, false>(*reinterpret_cast<const float4*>(&v[pp][k]), q4[c], a0, a1, a2, a3);
                 }
             } else if (rr < nnew) {                                // runtime row length (trace builds)
                 const uint4* row = reinterpret_cast<const uint4*>(base + (int64_t)rid[pp] * stride);
-                for (int c = j; c < nvr; c += 8) {
+                for (int c = j; c < nvr; c += L) {
                     const uint4 u = __ldg(row + c);
                     if constexpr (H16) acc8(u, q4[2 * c], q4[2 * c + 1], METRIC, a0, a1, a2, a3);
                     else acc4<METRIC, false>(*reinterpret_cast<const float4*>(&u), q4[c], a0, a1, a2, a3);
                 }
             }
             float sum = (a0 + a1) + (a2 + a3);
-            sum += __shfl_xor_sync(kFull, sum, 4);
-            sum += __shfl_xor_sync(kFull, sum, 2);
-            sum += __shfl_xor_sync(kFull, sum, 1);
-            const float t = __shfl_sync(kFull, sum, (lane & 3) << 3);
-            if ((lane >> 2) == p0 + pp) mine = t;
+#pragma unroll
+            for (int o = L / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+            const float t = __shfl_sync(kFull, sum, (lane % RPP) * L);
+            if (lane / RPP == p0 + pp) mine = t;
         }
     }
     return METRIC == 0 ? mine : -mine;

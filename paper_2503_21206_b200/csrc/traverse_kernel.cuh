@@ -34,7 +34,16 @@ constexpr int kTW = 4;                 // warps per block
 #ifndef PA_TRAV_MINB
 #define PA_TRAV_MINB 6                 // min resident blocks per SM (register budget 65536/(128·this))
 #endif
+#ifndef PA_TRAV_MINB_BLOOM
+#define PA_TRAV_MINB_BLOOM 8           // same, bloom visited set (3 KB of smem per warp instead of 8 KB)
+#endif
 constexpr int kIterCap = 1000000;      // Q16 safety cap (status 2)
+#ifndef PA_GROUP_L32
+#define PA_GROUP_L32 4                 // lanes per row in the distance gathers, fp32 rows
+#endif
+#ifndef PA_GROUP_L16
+#define PA_GROUP_L16 2                 // lanes per row, binary16 rows
+#endif
 
 // Bloom segment hash multipliers (odd; oracle O13 uses the same definition).
 __device__ __forceinline__ constexpr uint32_t bloom_mult(int j) {
@@ -360,7 +369,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
 //      or on the pending key before it is merged) and its row is fetched.
 // The expansion and visit sequences are identical to the sequential kernel.
 template <int METRIC, int VIS, int SMAX, int DPS4, bool TRACE, bool H16>
-__global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevIndex ix, SearchArgs a) {
+__global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_TRAV_MINB) k_traverse_pipe(DevIndex ix, SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ef = a.ef, dps = ix.rdim_pad, S = 1 << a.hash_log2;
@@ -401,7 +410,8 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse_pipe(DevInd
         __syncwarp();
         const int32_t cid = lane < nnew ? scr[lane] : 0;
         __syncwarp();
-        const float d = group_dists<METRIC, DPS4, H16>(qs, rows, stride, nvr, cid, nnew, lane);
+        const float d = group_dists<METRIC, DPS4, H16, H16 ? PA_GROUP_L16 : PA_GROUP_L32>(qs, rows, stride, nvr, cid,
+                                                                                          nnew, lane);
         return lane < nnew ? make_key(d, cid) : kKeyInf;
     };
 

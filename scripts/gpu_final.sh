@@ -7,7 +7,7 @@ if [ -z "$SKIP_TESTS" ]; then
 timeout 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/pytest_gpu.log
 fi
 timeout 1500 python bench.py --cache /tmp/pa_cache > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.log; echo "bench rc $?"
-python -c "import json;d=json.load(open('gpurun_out/bench_$TAG.json'));print({k:d[k] for k in ('value','ms_per_step','gpu_launches')}, d['roofline']['frac'], d['config']['ef'], d['config']['recall_at_10_gt_sub'], {k:(v['value'],v['ef'],v['traverse_ms']) for k,v in (d.get('f1_variants') or {}).items()}, (d.get('end_to_end_full') or {}).get('value'), d['e2e']['value'], d['cpu_baseline']['value'])"
+python -c "import json;d=json.load(open('gpurun_out/bench_$TAG.json'));print({k:d[k] for k in ('value','ms_per_step','gpu_launches')}, d['roofline']['frac'], d['config']['ef'], d['config']['recall_at_10_gt_sub'], {k:(v['value'],v['ef'],v['traverse_ms']) for k,v in (d.get('variants') or {}).items()}, (d.get('end_to_end_full') or {}).get('value'), d['e2e']['value'], d['cpu_baseline']['value'])"
 if [ -z "$SKIP_DIST" ]; then
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 3 --warmup 3 --no-full --no-cpu-baseline --no-f1 --cache /tmp/pa_cache > gpurun_out/bench_torchrun.json 2> gpurun_out/bench_torchrun.log; echo "torchrun rc $?"; cut -c1-300 gpurun_out/bench_torchrun.json
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 --cache /tmp/pa_cache > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.log; echo "reference rc $?"; cut -c1-300 gpurun_out/bench_reference.json
