@@ -103,6 +103,7 @@ struct FesParams {
     int sstride;                 // ≥ max cell size, multiple of 4
     int E;
     int32_t* entries;
+    bool fold_norm;              // pool_img carries ‖e‖² in K column dps (A has 1 there): acc = score
 };
 
 // Grouped GEMM: one CTA per (cell, 128 bucketed queries) tile; scores of the
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
     uint64_t* accf = empty + 2;
     uint64_t* acce = accf + 2;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(acce + 2);
+    float* nrm = reinterpret_cast<float*>(tslot + 4);        // 4 warps × 32 pool norms (unfolded L2)
 
     if (warp == 0) tmem_alloc(tslot, 2 * kN);
     if (tid == 0) {
@@ -258,13 +260,15 @@ __global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
             mbar_init(acce + i, kThreads);
         }
     }
-    if (warp < 4) {                                           // A: routed q' rows, hi/lo, swizzled
+    if (warp < 4) {                                           // A: routed [q', 1] rows, hi/lo, swizzled
         const int q = tid < nrows ? p.perm[pos0 + tid] : -1;
         for (int kc = 0; kc < kch; ++kc) {
 #pragma unroll 8
             for (int k = 0; k < 32; ++k) {
                 const int col = kc * 32 + k;
-                const float a = (q >= 0 && col < p.dps) ? __ldg(p.qp + (int64_t)q * p.dps + col) : 0.f;
+                const float a = q < 0 ? 0.f
+                              : col < p.dps ? __ldg(p.qp + (int64_t)q * p.dps + col)
+                              : (METRIC == 0 && p.fold_norm && col == p.dps ? 1.f : 0.f);
                 float hi, lo;
                 split_tf32(a, hi, lo);
                 const uint32_t off = (uint32_t)kc * 16384 + sw128_off(tid, k);
@@ -328,18 +332,18 @@ __global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
                 tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * kN + c0), v);
                 const int jb = j * kN + c0;
                 if (row < nrows && jb < nc) {
+                    if (METRIC == 0 && !p.fold_norm) {         // score = ‖e‖² + acc (acc = −2q'·e)
+                        float* nb = nrm + warp * 32;
+                        nb[lane] = jb + lane < nc ? __ldg(p.pool_norm + pb + jb + lane) : 0.f;
+                        __syncwarp();
 #pragma unroll
-                    for (int jj = 0; jj < 32; jj += 4) {
-                        float4 o;
-                        float* op = &o.x;
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int col = jb + jj + u;
-                            op[u] = METRIC == 0 ? fmaf(-2.f, v[jj + u], col < nc ? __ldg(p.pool_norm + pb + col) : 0.f)
-                                                : -v[jj + u];
-                        }
-                        if (jb + jj < nc) *reinterpret_cast<float4*>(srow + jb + jj) = o;
+                        for (int jj = 0; jj < 32; ++jj) v[jj] += nb[jj];
+                        __syncwarp();
                     }
+#pragma unroll
+                    for (int jj = 0; jj < 32; jj += 4)         // otherwise the accumulator IS the score
+                        if (jb + jj < nc)
+                            *reinterpret_cast<float4*>(srow + jb + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
                 }
             }
             tmem_fence_before();
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
     }
 }
 
-size_t fes_scores_tma_smem(int kch) { return (size_t)kch * 2 * 16384 + 2 * 32768 + 8 * 8 + 16; }
+size_t fes_scores_tma_smem(int kch) { return (size_t)kch * 2 * 16384 + 2 * 32768 + 8 * 8 + 16 + 512; }
 
 // Selection: one warp per bucketed query — E smallest (score, pool id) keys over
 // its cell's scores, kept sorted by the same threshold filter + rank merge as
@@ -738,7 +742,7 @@ int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
     p.perm = a.perm; p.qoff = a.qoff; p.toff = a.toff; p.r = ix.fes_r;
     p.pool_vec = ix.pool_vec; p.pool_norm = ix.pool_norm; p.pool_ids = ix.pool_ids; p.cell_off = ix.cell_off;
     p.metric = ix.metric; p.scores = a.fes_scores; p.sstride = ix.max_cell; p.E = a.E; p.entries = a.entries;
-    p.pool_img = ix.pool_img; p.chunk_off = ix.chunk_off;
+    p.pool_img = ix.pool_img; p.chunk_off = ix.chunk_off; p.fold_norm = ix.fes_fold_norm;
     const unsigned grid = (unsigned)((a.m + kM - 1) / kM + ix.fes_r);
     void* args[] = {&p};
     const char* ke = std::getenv("PA_FES_SCORES");

@@ -32,6 +32,7 @@ struct DevIndex {
     float* pool_img = nullptr;                 // [chunks][kch][hi,lo][4096]: pool split to TF32 hi/lo and laid
                                                // out as K-major SWIZZLE_128B 128×32 tiles (TMA bulk sources)
     int32_t* chunk_off = nullptr;              // [r+1] first 128-entry pool chunk of each cell
+    bool fes_fold_norm = false;                // pool_img rows are [−2e, ‖e‖²] (L2, spare K column) else −2e / −e
 };
 
 struct SearchArgs {

@@ -568,7 +568,13 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
         // Pre-split, pre-swizzled pool tiles for the TMA-fed tcgen05 FES GEMM:
         // per cell, per 128-entry chunk, per 32-float K chunk: hi tile then lo tile,
         // element (row, k) at the K-major SWIZZLE_128B offset used by the kernel.
+        // The score epilogue is folded into the GEMM: B row = [−2e, ‖e‖²] (L2; the
+        // A row carries a 1 in column dps) or [−e] (IP), so the accumulator IS the
+        // GEMM-form score ‖e‖² − 2q'·e / −q'·e.
+        // (L2 needs a spare K column: d' a multiple of 32 keeps ‖e‖² in the epilogue.)
+        const bool l2 = p->metric == PA_L2;
         const int kch = (dps + 31) / 32;
+        d.fes_fold_norm = l2 && (dps % 32) != 0;
         std::vector<int32_t> choff(r + 1, 0);
         for (int c = 0; c < r; ++c)
             choff[c + 1] = choff[c] + (int32_t)((p->fes_cell_off[c + 1] - p->fes_cell_off[c] + 127) / 128);
@@ -586,7 +592,8 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
                     float* lo = &img[(((size_t)ch * kch + kc) * 2 + 1) * 4096];
                     for (int k = 0; k < 32; ++k) {
                         const int col = kc * 32 + k;
-                        const float a = col < dp ? src[col] : 0.f;
+                        const float a = col < dp ? (l2 ? -2.f * src[col] : -src[col])
+                                                 : (d.fes_fold_norm && col == dps ? pn[b + e] : 0.f);
                         uint32_t bits;
                         std::memcpy(&bits, &a, 4);
                         bits &= 0xFFFFE000u;
