@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
     uint64_t* acce = accf + 2;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(acce + 2);
     float* nrm = reinterpret_cast<float*>(tslot + 4);        // 4 warps × 32 pool norms (unfolded L2)
+    float* stg = nrm + 128;                                   // 4 warps × 32 × 36 floats: store staging
 
     if (warp == 0) tmem_alloc(tslot, 2 * kN);
     if (tid == 0) {
@@ -321,8 +322,10 @@ __global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
         }
         __syncwarp();
     } else {
-        const int row = tid;
-        float* srow = p.scores + (int64_t)(pos0 + row) * p.sstride;
+        // Epilogue: thread t holds row t of each 32-column block (tcgen05.ld); the
+        // block goes through smem so that every global store instruction writes
+        // whole 128-B lines of 4 rows instead of 16 B of 32 rows.
+        float* tile = stg + warp * (32 * 36);                 // 32 rows × 32 floats, row stride 36
         for (int j = 0; j < nchunk; ++j) {
             const int acc = j & 1;
             mbar_wait(accf + acc, (j >> 1) & 1);
@@ -331,19 +334,26 @@ __global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
                 float v[32];
                 tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * kN + c0), v);
                 const int jb = j * kN + c0;
-                if (row < nrows && jb < nc) {
-                    if (METRIC == 0 && !p.fold_norm) {         // score = ‖e‖² + acc (acc = −2q'·e)
-                        float* nb = nrm + warp * 32;
-                        nb[lane] = jb + lane < nc ? __ldg(p.pool_norm + pb + jb + lane) : 0.f;
-                        __syncwarp();
+                if (jb >= nc) continue;                        // warp-uniform
+                float* nb = nrm + warp * 32;                   // unfolded L2: score = ‖e‖² + acc (acc = −2q'·e)
+                __syncwarp();
+                if (METRIC == 0 && !p.fold_norm) {
+                    nb[lane] = jb + lane < nc ? __ldg(p.pool_norm + pb + jb + lane) : 0.f;
+                    __syncwarp();
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) v[jj] += nb[jj];
-                        __syncwarp();
-                    }
+                    for (int jj = 0; jj < 32; ++jj) v[jj] += nb[jj];
+                }                                              // otherwise the accumulator IS the score
 #pragma unroll
-                    for (int jj = 0; jj < 32; jj += 4)         // otherwise the accumulator IS the score
-                        if (jb + jj < nc)
-                            *reinterpret_cast<float4*>(srow + jb + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+                for (int jj = 0; jj < 32; jj += 4)
+                    *reinterpret_cast<float4*>(tile + lane * 36 + jj) = make_float4(v[jj], v[jj + 1], v[jj + 2], v[jj + 3]);
+                __syncwarp();
+                const int cc = (lane & 7) * 4;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int rl = i * 4 + (lane >> 3), rg = warp * 32 + rl;
+                    if (rg < nrows && jb + cc < nc)
+                        *reinterpret_cast<float4*>(p.scores + (int64_t)(pos0 + rg) * p.sstride + jb + cc) =
+                            *reinterpret_cast<const float4*>(tile + rl * 36 + cc);
                 }
             }
             tmem_fence_before();
@@ -358,7 +368,9 @@ __global__ void __launch_bounds__(160, 1) k_fes_scores_tma(FesParams p) {
     }
 }
 
-size_t fes_scores_tma_smem(int kch) { return (size_t)kch * 2 * 16384 + 2 * 32768 + 8 * 8 + 16 + 512; }
+size_t fes_scores_tma_smem(int kch) {
+    return (size_t)kch * 2 * 16384 + 2 * 32768 + 8 * 8 + 16 + 512 + 4 * 32 * 36 * 4;
+}
 
 // Selection: one warp per bucketed query — E smallest (score, pool id) keys over
 // its cell's scores, kept sorted by the same threshold filter + rank merge as

@@ -4,7 +4,7 @@ mkdir -p gpurun_out; rm -rf /tmp/pa_cache
 TAG=${1:-it}
 python __graft_entry__.py > gpurun_out/build.log 2>&1
 if [ -z "$SKIP_TESTS" ]; then
-timeout 1500 python -m pytest tests -m gpu -q -rf -x ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc $?"; tail -3 gpurun_out/pytest_gpu_$TAG.log
+timeout 900 python -m pytest tests -m gpu -q -rf -x --timeout 300 ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc $?"; tail -3 gpurun_out/pytest_gpu_$TAG.log
 fi
 timeout 1200 python bench.py --steps 10 --warmup 3 --no-cpu-baseline ${BENCH_ARGS} --cache /tmp/pa_cache > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.log; echo "bench rc $?"
 python -c "import json;d=json.load(open('gpurun_out/bench_$TAG.json'));print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['kernel_ms'], d['config']['ef'], d['config']['recall_at_10_gt_sub']); [print(k, v['value'], v['ef'], v['traverse_ms'], v['roofline_frac'], v['recall_at_10_gt_sub'], round(v['n_dist_per_q'],1)) for k,v in (d.get('variants') or {}).items()]; print('full', (d.get('end_to_end_full') or {}).get('value'), 'e2e', d['e2e']['value'])"
