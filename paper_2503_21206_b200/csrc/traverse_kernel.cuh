@@ -410,8 +410,8 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
         __syncwarp();
         const int32_t cid = lane < nnew ? scr[lane] : 0;
         __syncwarp();
-        const float d = group_dists<METRIC, DPS4, H16, H16 ? PA_GROUP_L16 : PA_GROUP_L32>(qs, rows, stride, nvr, cid,
-                                                                                          nnew, lane);
+        const float d = group_dists<METRIC, DPS4, H16, H16 ? PA_GROUP_L16 : PA_GROUP_L32, VIS != 2>(
+            qs, rows, stride, nvr, cid, nnew, lane);
         return lane < nnew ? make_key(d, cid) : kKeyInf;
     };
 
