@@ -371,6 +371,18 @@ def run_ours(args, rank, world, local_rank):
     full = None
     if not args.no_full:
         full = measure_full(ix, inst, cfg, args, rank)
+    # ---- NEXT-f4: Table 6 ablation — components removed cumulatively
+    ablation = None
+    if args.ablation:
+        ablation = []
+        fl = 0
+        for name, bit in (("full", 0), ("-pipelining", pa.PA_NO_PIPELINE), ("-FES", pa.PA_NO_FES),
+                          ("-stage2", pa.PA_NO_STAGE2), ("-stage1", pa.PA_NO_STAGE1)):
+            fl |= bit
+            r_ = measure_full(ix, inst, cfg, args, rank, flags=fl)
+            ablation.append({"removed": name, "flags": fl, "qps_at_0.90": r_["value"], "ef": r_["ef"],
+                             "sweep": r_["sweep"]})
+            log(f"[rank {rank}] ablation {name}: {r_['value']} q/s ef={r_['ef']}")
 
     peak, peak_src = measured_peaks()
     achieved = bytes_alg / (trav / 1e3) / 1e9
@@ -405,6 +417,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": {"value": round(e2e_qps, 1), "unit": "queries/s", "h2d_bytes_per_step": m * cfg.D * 4,
                     "d2h_bytes_per_step": m * k * 8},
             "end_to_end_full": full,
+            "ablation_table6": ablation,
             "variants": variants,
             "gpu_launches": launches,
             "clocks": clocks,
@@ -413,7 +426,7 @@ def run_ours(args, rank, world, local_rank):
     ix.close()
 
 
-def measure_full(ix, inst, cfg, args, rank):
+def measure_full(ix, inst, cfg, args, rank, flags=0):
     """M1: pa_search(PA_STAGES_FULL) — GPU stage ① + host ② ③ — against full-space GT."""
     import paper_2503_21206_b200 as pa
     k = cfg.k
@@ -422,9 +435,10 @@ def measure_full(ix, inst, cfg, args, rank):
     sweep = []
     hq = inst["queries"]
     for ef in (16, 32, 64, 128, 192, 256):
-        ix.search(hq, k=k, ef=ef, stages=pa.PA_STAGES_FULL, bloom_log2=args.bloom)              # warm-up (pinned buffers, pools)
+        kw = dict(stages=pa.PA_STAGES_FULL, bloom_log2=args.bloom, flags=flags)
+        ix.search(hq, k=k, ef=ef, **kw)                                 # warm-up (pinned buffers, pools)
         t = time.perf_counter()
-        ids, _ = ix.search(hq, k=k, ef=ef, stages=pa.PA_STAGES_FULL, bloom_log2=args.bloom)
+        ids, _ = ix.search(hq, k=k, ef=ef, **kw)
         dt = time.perf_counter() - t
         rec = recall_at(ids, inst["gt_ids"], k)
         st = ix.stats()
@@ -472,6 +486,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--full-sweep", action="store_true")
     ap.add_argument("--no-full", action="store_true")
+    ap.add_argument("--ablation", action="store_true", help="NEXT-f4: Table 6 cumulative ablation of the full pipeline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-f1", action="store_true", help="skip the binary16-storage (NEXT-f1) variant")
     ap.add_argument("--cache", default=None, help="dir to cache the generated instance (same-call reuse only)")

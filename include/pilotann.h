@@ -63,6 +63,8 @@ enum {
     PA_NO_FES = 1u,    /* entries = the first E pool ids in pool order (no routing / scoring)   */
     PA_NO_STAGE2 = 2u, /* carry = stage-① candidates re-ranked by full δ, visited = their ids      */
     PA_NO_STAGE1 = 4u, /* stage-① output = the entries themselves (no subgraph traversal)        */
+    PA_NO_PIPELINE = 8u, /* PA_STAGES_FULL: run the GPU stage over the whole batch before the host
+                            stages start (no CPU–GPU overlap, Table 6 "−pipelining"); results identical */
 };
 
 typedef struct pa_index pa_index; /* opaque */

@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "PA_OK", -1: "PA_EINVAL", -2: "PA_EGRAPH", -3: "PA_EBASIS", -
                 -5: "PA_ENOMEM", -6: "PA_ECUDA", -7: "PA_ESTATE", -8: "PA_ENOTSUP"}
 PA_L2, PA_IP = 0, 1
 PA_STAGES_GPU, PA_STAGES_FULL = 1, 3
-PA_NO_FES, PA_NO_STAGE2, PA_NO_STAGE1 = 1, 2, 4
+PA_NO_FES, PA_NO_STAGE2, PA_NO_STAGE1, PA_NO_PIPELINE = 1, 2, 4, 8
 
 # Symbols declared in include/pilotann.h (checked by tests/test_abi.py).
 EXPORTS = ("pa_build", "pa_attach_host", "pa_search", "pa_search_device", "pa_search_candidates",

@@ -592,8 +592,14 @@ __global__ void __launch_bounds__(128) k_fes_select2(FesParams p, int64_t m) {
 //   * ≤ 128 candidates are sorted in registers; larger sets take the smem sort,
 //     more than kSelCap (heavy ties) the rank-merge fallback.
 // Keys and hence entries are identical to k_fes_select / k_fes_select2.
+#ifndef PA_SEL_MINB
+#define PA_SEL_MINB 6
+#endif
+#ifndef PA_SEL_NV
+#define PA_SEL_NV 8
+#endif
 template <int KPMAX, int SMAX, int NV>
-__global__ void __launch_bounds__(128) k_fes_select3(FesParams p, int64_t m) {
+__global__ void __launch_bounds__(128, PA_SEL_MINB) k_fes_select3(FesParams p, int64_t m) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // 2·ceil(E/32) words per lane: a lane rarely holds more of the row's E smallest
@@ -776,9 +782,10 @@ int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
         sel = a.E <= 64 ? (void*)k_fes_select<2> : a.E <= 128 ? (void*)k_fes_select<4> : (void*)k_fes_select<8>;
         ssm = (size_t)4 * a.E * 8;
     } else if (!(se && !std::strcmp(se, "two-pass"))) {
-        sel = a.E <= 32 ? (void*)k_fes_select3<2, 2, 8> : a.E <= 64 ? (void*)k_fes_select3<4, 2, 8>
-            : a.E <= 96 ? (void*)k_fes_select3<6, 4, 8> : a.E <= 128 ? (void*)k_fes_select3<8, 4, 8>
-            : (void*)k_fes_select3<16, 8, 8>;
+        constexpr int NV = PA_SEL_NV;
+        sel = a.E <= 32 ? (void*)k_fes_select3<2, 2, NV> : a.E <= 64 ? (void*)k_fes_select3<4, 2, NV>
+            : a.E <= 96 ? (void*)k_fes_select3<6, 4, NV> : a.E <= 128 ? (void*)k_fes_select3<8, 4, NV>
+            : (void*)k_fes_select3<16, 8, NV>;
         ssm = (size_t)4 * kSelCap * 8;
     } else {
         sel = a.E <= 64 ? (void*)k_fes_select2<2, 2> : a.E <= 96 ? (void*)k_fes_select2<3, 4>

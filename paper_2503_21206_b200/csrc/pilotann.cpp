@@ -685,7 +685,7 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
     if (st != PA_OK) return st;
     const auto& d = ix->dev;
     // Stages ②③ pipeline over sub-batches (GPU stage of batch j+1 overlaps host work on j).
-    const int64_t bsz = full ? std::max<int64_t>(1024, (m + 7) / 8) : m;
+    const int64_t bsz = full && !(r.flags & PA_NO_PIPELINE) ? std::max<int64_t>(1024, (m + 7) / 8) : m;
     const int64_t nb = (m + bsz - 1) / bsz;
     if (full) {
         st = ensure_pipe_events(ix, nb);

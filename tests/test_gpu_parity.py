@@ -351,3 +351,14 @@ def test_bloom_rejects_bad_sizes(s1):
             run_gpu(ix, s1, 10, 64, bloom_log2=bl)
         assert e.value.status == pa.PA_EINVAL
     ix.close()
+
+
+def test_no_pipeline_toggle_is_result_identical(s1):
+    """PA_NO_PIPELINE (Table 6 '-pipelining') only removes the CPU–GPU overlap."""
+    cfg = s1["cfg"]
+    ix = pa.Index.from_instance(s1)
+    ix.attach_host(s1["full_offsets"], s1["full_neighbors"], s1["rotated"])
+    a = ix.search(s1["queries"], k=cfg.k, ef=cfg.ef, stages=pa.PA_STAGES_FULL)
+    b = ix.search(s1["queries"], k=cfg.k, ef=cfg.ef, stages=pa.PA_STAGES_FULL, flags=pa.PA_NO_PIPELINE)
+    ix.close()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
