@@ -106,12 +106,25 @@ def measured_peaks():
 
 
 # --------------------------------------------------------------- instance --
-def make_instance(cfg_name, world, rank, m_per_rank, cache=None):
+def parse_overrides(items):
+    """--set key=value pairs → typed Config overrides (NEXT-f2 operating points)."""
+    out = {}
+    for it in items or []:
+        k, v = it.split("=", 1)
+        out[k] = float(v) if "." in v else int(v)
+    return out
+
+
+def make_instance(cfg_name, world, rank, m_per_rank, cache=None, overrides=None):
     import torch
     import datagen as dg
-    cfg = dg.get_config(cfg_name, m=m_per_rank * world)
+    ov = dict(overrides or {})
+    cfg = dg.get_config(cfg_name, m=m_per_rank * world, **ov)
+    if ov:
+        cfg.name += "[" + ",".join(f"{k}={v}" for k, v in sorted(ov.items())) + "]"
     t0 = time.time()
-    path = os.path.join(cache, f"inst_{cfg_name}_{world}_{rank}_{m_per_rank}.npz") if cache else None
+    tag = "_".join(f"{k}{v}" for k, v in sorted(ov.items()))
+    path = os.path.join(cache, f"inst_{cfg_name}{tag}_{world}_{rank}_{m_per_rank}.npz") if cache else None
     if path and os.path.exists(path):
         z = np.load(path, allow_pickle=False)
         inst = {k: z[k] for k in z.files}
@@ -159,7 +172,8 @@ def run_reference(args, rank, world):
     import oracle as orc
     orc.build()
     torch.cuda.set_device(0) if torch.cuda.is_available() else None
-    cfg, inst = make_instance(args.config, 1, 0, args.m, args.cache) if torch.cuda.is_available() else make_cpu_instance(args)
+    cfg, inst = make_instance(args.config, 1, 0, args.m, args.cache, parse_overrides(args.set)) \
+        if torch.cuda.is_available() else make_cpu_instance(args)
     cores = os.cpu_count()
     sample = args.ref_sample
     Q = inst["queries"]
@@ -197,7 +211,7 @@ def run_reference(args, rank, world):
 
 def make_cpu_instance(args):
     import datagen as dg
-    cfg = dg.get_config(args.config, m=args.m)
+    cfg = dg.get_config(args.config, m=args.m, **parse_overrides(args.set))
     return cfg, dg.build_instance(cfg)
 
 
@@ -211,7 +225,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    cfg, inst = make_instance(args.config, world, rank, args.m, args.cache)
+    cfg, inst = make_instance(args.config, world, rank, args.m, args.cache, parse_overrides(args.set))
     k = cfg.k
     m = inst["queries"].shape[0]
     t0 = time.time()
@@ -229,6 +243,8 @@ def run_ours(args, rank, world, local_rank):
     out_d = torch.empty(m, k, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    gt_key = "gt_sub_ids" if args.gt == "sub" else "gt_ids"     # operating-point rule's ground truth
+
     def step(ef):
         ix.search_device(qd, k, ef, out_i, out_d, stream=stream.cuda_stream, bloom_log2=args.bloom)
 
@@ -238,7 +254,7 @@ def run_ours(args, rank, world, local_rank):
     for ef in ([args.ef] if args.ef else EF_SWEEP):
         step(ef)
         torch.cuda.synchronize()
-        rec = recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k)
+        rec = recall_at(out_i.cpu().numpy(), inst[gt_key], k)
         st = ix.stats()
         sweep.append({"ef": ef, "recall_at_10": round(rec, 4), "gpu_ms": round(st["ms_total_gpu"], 3),
                       "n_dist_per_q": st["sum_n_dist"] / m, "n_exp_per_q": st["sum_n_exp"] / m})
@@ -313,7 +329,7 @@ def run_ours(args, rank, world, local_rank):
         for e in EF_SWEEP:
             stepv(e)
             torch.cuda.synchronize()
-            if recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k) >= TARGET_RECALL:
+            if recall_at(out_i.cpu().numpy(), inst[gt_key], k) >= TARGET_RECALL:
                 efv = e
                 break
         efv = efv or EF_SWEEP[-1]
@@ -322,7 +338,7 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             efv = int(t.item())
         v = timed(stepv, ixv, efv, fp16)
-        rv = recall_at(out_i.cpu().numpy(), inst["gt_sub_ids"], k)
+        rv = recall_at(out_i.cpu().numpy(), inst[gt_key], k)
         pk, _ = measured_peaks()
         ach = v["bytes"] / (v["trav_ms"] / 1e3) / 1e9
         if fp16:
@@ -393,7 +409,8 @@ def run_ours(args, rank, world, local_rank):
         cpu = None if args.no_cpu_baseline else cpu_baseline(oinst, cfg, ef, args)
         clocks = clk.summary()
         line = {
-            "metric": "QPS at Recall@10=0.90 (GPU stage: projection+FES+subgraph traversal, GT_sub)",
+            "metric": "QPS at Recall@10=0.90 (GPU stage: projection+FES+subgraph traversal, "
+                      + ("GT_sub)" if args.gt == "sub" else "full-space GT)"),
             "value": round(qps, 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -486,6 +503,11 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--full-sweep", action="store_true")
     ap.add_argument("--no-full", action="store_true")
+    ap.add_argument("--gt", default="sub", choices=["sub", "full"],
+                    help="ground truth of the Recall@10 >= 0.90 rule: the sampled subgraph's (stage-1 target) or "
+                         "full-space (GPU-only operating points, NEXT-f2)")
+    ap.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
+                    help="override a datagen Config field (e.g. ratio=1.0, dp=96: NEXT-f2 operating points)")
     ap.add_argument("--ablation", action="store_true", help="NEXT-f4: Table 6 cumulative ablation of the full pipeline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-f1", action="store_true", help="skip the binary16-storage (NEXT-f1) variant")

@@ -613,8 +613,12 @@ def build_instance(cfg: Config, device="cpu", with_full_graph: bool = True, gt: 
     full_rows = build_graph(X, cfg.R, labels=lab) if cfg.shape == "mixture" else knn_graph(X, cfg.R, labels=lab)
     full_off, full_nbrs = csr_from_rows(full_rows.cpu().numpy(), cfg.N)
     del full_rows
-    flags = sample_members(full_off, full_nbrs, cfg.ratio, cfg.seeds["sample"])
-    sub_off, sub_nbrs = reconnect(X, flags, cfg.R, labels=lab, plain_knn=cfg.shape != "mixture")
+    if cfg.ratio >= 1.0:             # every node sampled: reconnecting with the same construction IS the full graph
+        flags = np.ones(cfg.N, np.uint8)
+        sub_off, sub_nbrs = full_off, full_nbrs
+    else:
+        flags = sample_members(full_off, full_nbrs, cfg.ratio, cfg.seeds["sample"])
+        sub_off, sub_nbrs = reconnect(X, flags, cfg.R, labels=lab, plain_knn=cfg.shape != "mixture")
     V = fit_svd(X, cfg.seeds["base"])
     Xh = rotate(X, V)
     del X

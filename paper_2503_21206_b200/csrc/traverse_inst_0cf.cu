@@ -23,6 +23,7 @@ void* pick4p(int d, bool trace) {
         case 32: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 8, false, false>;
         case 48: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 12, false, false>;
         case 64: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 16, false, false>;
+        case 96: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 24, false, false>;
         case 128: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 32, false, false>;
         default: return (void*)k_traverse_pipe<METRIC, VIS, SMAX, 0, false, false>;
     }

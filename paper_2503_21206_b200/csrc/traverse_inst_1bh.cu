@@ -12,6 +12,7 @@ void* pick4p(int d, bool trace) {
         case 32: return (void*)k_traverse_pipe<METRIC, 2, SMAX, 4, false, true>;
         case 48: return (void*)k_traverse_pipe<METRIC, 2, SMAX, 6, false, true>;
         case 64: return (void*)k_traverse_pipe<METRIC, 2, SMAX, 8, false, true>;
+        case 96: return (void*)k_traverse_pipe<METRIC, 2, SMAX, 12, false, true>;
         case 128: return (void*)k_traverse_pipe<METRIC, 2, SMAX, 16, false, true>;
         default: return (void*)k_traverse_pipe<METRIC, 2, SMAX, 0, false, true>;
     }
