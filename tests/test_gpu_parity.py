@@ -271,14 +271,15 @@ def test_fp16_storage_full_pipeline(s1):
 
 @pytest.mark.parametrize("cfg_name", ["S1", "S2", "C0"])
 def test_fes_selection_variants_agree(cfg_name, request, monkeypatch):
-    """The latency-restructured selection (default), the two-pass (threshold +
-    single sort) selection and the rank-merge selection return exactly the same
-    entries (same GEMM scores, same keys)."""
+    """The group-minima selection (default), the per-lane top-KP selection
+    (select3), the two-pass (threshold + single sort) selection and the
+    rank-merge selection return exactly the same entries (same GEMM scores,
+    same keys)."""
     inst = request.getfixturevalue(cfg_name.lower())
     cfg = inst["cfg"]
     ix = pa.Index.from_instance(inst)
     outs = []
-    for sel in ("default", "two-pass", "merge"):
+    for sel in ("default", "select3", "two-pass", "merge"):
         if sel == "default":
             monkeypatch.delenv("PA_FES_SELECT", raising=False)
         else:
