@@ -83,14 +83,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def ncu_traffic(workload, ef, kernel="k_traverse"):
+def ncu_traffic(workload, ef, bloom=0, kernel="k_traverse"):
     """DRAM bytes per launch of `kernel` from a committed `ncu --set full` capture
-    (profiles/ncu_traffic.json), when one exists for this workload and ef."""
+    (profiles/ncu_traffic.json), when one exists for this workload, ef and visited set."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(workload, {}).get(str(ef))
+        e = d.get(workload, {}).get(str(ef) + (f"_bloom{bloom}" if bloom else ""))
         return (e["dram_bytes"], e["source"]) if e and e.get("kernel") == kernel else (None, None)
     except (OSError, ValueError, KeyError):
         return None, None
@@ -402,7 +402,7 @@ def run_ours(args, rank, world, local_rank):
 
     peak, peak_src = measured_peaks()
     achieved = bytes_alg / (trav / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic(cfg.name, ef)
+    traffic, traffic_src = ncu_traffic(cfg.name, ef, args.bloom)
     line = None
     if rank == 0:
         oinst = inst if args.reduced == "fp32" else dict(inst, reduced=inst["reduced"].astype(np.float16).astype(np.float32))
