@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -777,31 +778,39 @@ __global__ void __launch_bounds__(128, 4) k_fes_select4(FesParams p, int64_t m) 
 #pragma unroll
             for (int k = 0; k < 4; ++k) wd[k] = (i4 * 4 + k < nc) ? ord_of(f[k]) : 0xffffffffu;
         };
-        // ---- pass 1: group minima
-        uint32_t mn[16];
+        // ---- pass 1: group minima (fminf on the scores, ordered word of the minimum only)
+        const float kInf = __int_as_float(0x7f800000);
+        float fm[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) mn[i] = 0xffffffffu;
+        for (int i = 0; i < 16; ++i) fm[i] = kInf;
 #pragma unroll
         for (int t0 = 0; t0 < NT; t0 += 8) {
+            if (t0 * 32 >= n4) break;                      // warp-uniform
             float4 v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int i4 = (t0 + u) * 32 + lane;
-                v[u] = i4 < n4 ? srow4[i4] : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[u] = i4 < n4 ? srow4[i4] : make_float4(kInf, kInf, kInf, kInf);
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int i4 = (t0 + u) * 32 + lane;
-                uint32_t wd[4];
-                word4(v[u], i4, wd);
-                const uint32_t a = min(min(wd[0], wd[1]), min(wd[2], wd[3]));
-                if (i4 < n4) mn[(t0 + u) / G] = min(mn[(t0 + u) / G], a);
+                float4 x = v[u];
+                if (i4 * 4 + 3 >= nc) {                    // ragged tail of the cell
+                    if (i4 * 4 + 1 >= nc) x.y = kInf;
+                    if (i4 * 4 + 2 >= nc) x.z = kInf;
+                    if (i4 * 4 + 3 >= nc) x.w = kInf;
+                }
+                fm[(t0 + u) / G] = fminf(fm[(t0 + u) / G], fminf(fminf(x.x, x.y), fminf(x.z, x.w)));
             }
         }
+        uint32_t mn[16];                                   // ord is monotone: ord(min) = min(ord)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mn[i] = ord_of(fm[i]);
         uint32_t T = 0xffffffffu;
         if (nc > E) {
             uint32_t lo = 0;                              // largest prefix with count(< prefix) < E
-            for (int b = 31; b >= 8; --b) {
+            for (int b = 31; b >= 12; --b) {
                 const uint32_t trial = lo | (1u << b);
                 int cnt = 0;
 #pragma unroll
@@ -809,7 +818,7 @@ __global__ void __launch_bounds__(128, 4) k_fes_select4(FesParams p, int64_t m) 
                 cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
                 if (cnt < E) lo = trial;
             }
-            T = lo | 0xffu;                               // count(minima ≤ T) ≥ E
+            T = lo | 0xfffu;                              // count(minima ≤ T) ≥ E
         }
         // ---- pass 2: indices of the entries with word ≤ T, by warp prefix sums
         int M = 0;
@@ -861,17 +870,23 @@ __global__ void __launch_bounds__(128, 4) k_fes_select4(FesParams p, int64_t m) 
             }
             __syncwarp();
         }
-        if (!overflow && M <= 128) {
-            uint64_t t4[4];
+        auto sort_regs = [&](auto tag) {
+            constexpr int K = decltype(tag)::value;
+            uint64_t tk[K];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) t4[a] = a * 32 + lane < M ? buf[a * 32 + lane] : kKeyInf;
-            warp_bitonic_regs<4>(t4, lane);
+            for (int a = 0; a < K; ++a) tk[a] = a * 32 + lane < M ? buf[a * 32 + lane] : kKeyInf;
+            warp_bitonic_regs<K>(tk, lane);
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
+            for (int a = 0; a < K; ++a) {
                 const int j = a * 32 + lane;
-                if (j < E) p.entries[(int64_t)q * E + j] = j < M ? key_id(t4[a]) : -1;
+                if (j < E) p.entries[(int64_t)q * E + j] = j < M ? key_id(tk[a]) : -1;
             }
-            for (int j = 128 + lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = -1;
+            for (int j = 32 * K + lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = -1;
+        };
+        if (!overflow && M <= 128) {
+            sort_regs(std::integral_constant<int, 4>{});
+        } else if (!overflow && M <= 256) {
+            sort_regs(std::integral_constant<int, 8>{});
         } else if (!overflow) {
             int n2 = 32;
             while (n2 < M) n2 <<= 1;
