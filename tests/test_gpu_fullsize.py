@@ -27,11 +27,13 @@ def c1():
     return dg.build_instance(cfg, device="cuda", gt=False)
 
 
-@pytest.mark.parametrize("ef", [32, 128])
-def test_c1_full_size_sampled_parity(c1, ef):
+@pytest.mark.parametrize("ef,bloom", [(32, 0), (128, 0), (96, 12)])
+def test_c1_full_size_sampled_parity(c1, ef, bloom):
+    """(96, 12) is bench.py's headline launch: ef 96 with the paper's bloom
+    visited set of 3 × 2^12 bits, checked against the oracle's O13 mode."""
     cfg = c1["cfg"]
     ix = pa.Index.from_instance(c1)
-    g = run_gpu(ix, c1, cfg.k, ef, trace_cap=6144)
+    g = run_gpu(ix, c1, cfg.k, ef, trace_cap=6144, bloom_log2=bloom)
     ix.close()
     m = c1["queries"].shape[0]
     assert m == 10_000 and np.all(g["status"] == 0)
@@ -45,9 +47,9 @@ def test_c1_full_size_sampled_parity(c1, ef):
     sample = np.arange(0, m, 50)
     sub = dict(c1, queries=c1["queries"][sample])
     gs = {k: v[sample] for k, v in g.items()}
-    r = orc.search(sub, k=cfg.k, ef=ef, stages=1, trace_cap=6144)
+    r = orc.search(sub, k=cfg.k, ef=ef, stages=1, trace_cap=6144, bloom_log2=bloom or None)
     rep = compare(sub, gs, r, cfg.k, ef)
-    print(f"C1 ef={ef}", rep)
+    print(f"C1 ef={ef} bloom={bloom}", rep)
     assert not rep.fail, rep.fail[:5]
     assert rep.exact >= 0.8 * sample.size
     # distances of every returned id on all queries vs fp64 (vectorised property check)
