@@ -56,6 +56,9 @@ typedef enum { PA_L2 = 0, PA_IP = 1 } pa_metric;
 typedef enum {
     PA_STAGES_GPU = 1,  /* stage ① only: FES + subgraph traversal on reduced vectors (§4.1 ①, §5)  */
     PA_STAGES_FULL = 3, /* ① on the GPU, then ② residual refinement and ③ final traversal on host   */
+    PA_STAGES_FULL_GPU = 7, /* NEXT-f3: ①②③ all on the GPU (O8-O9 semantics, exact visited sets in ②③);
+                               needs pa_attach_host, whose full graph (degree ≤ 64) and X̂ are copied to
+                               the device on first use (PA_ENOMEM if they do not fit) */
 } pa_stages;
 
 /* Ablation toggles (Table 6). */
@@ -137,7 +140,8 @@ typedef struct {
     double ms_h2d, ms_d2h, ms_host_stages, ms_wall;      /* host-observed                  */
     int64_t sum_n_exp, sum_n_dist, sum_spill;            /* stage ① counters, summed        */
     int64_t overflow_queries;                            /* queries that hit a cap           */
-    int64_t sum_n_dist2, sum_n_dist3;                    /* host stages ②③                 */
+    int64_t sum_n_dist2, sum_n_dist3;                    /* stages ②③ (host, or GPU)       */
+    double ms_refine;                                    /* PA_STAGES_FULL_GPU: ②③ kernel  */
 } pa_stats;
 
 /* Build one device replica.  Validates every input (PA_EINVAL / PA_EGRAPH /

@@ -26,7 +26,7 @@ PA_OK, PA_EINVAL, PA_EGRAPH, PA_EBASIS, PA_EFES, PA_ENOMEM, PA_ECUDA, PA_ESTATE,
 STATUS_NAMES = {0: "PA_OK", -1: "PA_EINVAL", -2: "PA_EGRAPH", -3: "PA_EBASIS", -4: "PA_EFES",
                 -5: "PA_ENOMEM", -6: "PA_ECUDA", -7: "PA_ESTATE", -8: "PA_ENOTSUP"}
 PA_L2, PA_IP = 0, 1
-PA_STAGES_GPU, PA_STAGES_FULL = 1, 3
+PA_STAGES_GPU, PA_STAGES_FULL, PA_STAGES_FULL_GPU = 1, 3, 7
 PA_NO_FES, PA_NO_STAGE2, PA_NO_STAGE1, PA_NO_PIPELINE = 1, 2, 4, 8
 
 # Symbols declared in include/pilotann.h (checked by tests/test_abi.py).
@@ -68,7 +68,8 @@ class Stats(C.Structure):
                 ("ms_total_gpu", C.c_double), ("ms_h2d", C.c_double), ("ms_d2h", C.c_double),
                 ("ms_host_stages", C.c_double), ("ms_wall", C.c_double),
                 ("sum_n_exp", C.c_int64), ("sum_n_dist", C.c_int64), ("sum_spill", C.c_int64),
-                ("overflow_queries", C.c_int64), ("sum_n_dist2", C.c_int64), ("sum_n_dist3", C.c_int64)]
+                ("overflow_queries", C.c_int64), ("sum_n_dist2", C.c_int64), ("sum_n_dist3", C.c_int64),
+                ("ms_refine", C.c_double)]
 
     def asdict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -32,6 +32,11 @@ struct DevIndex {
     float* pool_img = nullptr;                 // [chunks][kch][hi,lo][4096]: pool split to TF32 hi/lo and laid
                                                // out as K-major SWIZZLE_128B 128×32 tiles (TMA bulk sources)
     int32_t* chunk_off = nullptr;              // [r+1] first 128-entry pool chunk of each cell
+    // NEXT-f3 (PA_STAGES_FULL_GPU), uploaded on first use from pa_attach_host's arrays
+    int32_t* full_ell = nullptr;               // [n][full_w] full graph, −1 padded
+    int32_t full_w = 0;
+    float* xhat = nullptr;                     // [n][xstride] rotated full vectors X̂ (xstride: D rounded to 32)
+    int32_t xstride = 0;
     bool fes_fold_norm = false;                // pool_img rows are [−2e, ‖e‖²] (L2, spare K column) else −2e / −e
 };
 
@@ -68,6 +73,32 @@ struct SearchArgs {
     int32_t* trace_nexp = nullptr;
     int32_t* trace_nvis = nullptr;
 };
+
+// Stages ②③ on the GPU (NEXT-f3, k_refine).
+struct Refine23 {
+    int64_t m = 0;
+    int32_t k = 10, ef1 = 64, ef2 = 32, ef3 = 64, refine_iters = 2;
+    uint32_t flags = 0;
+    int32_t D = 0, dp = 0, qlen = 0, qp_stride = 0;
+    const float* qp = nullptr;          // [m][qp_stride] q'
+    const float* qres = nullptr;        // [m][D − d'] q_res
+    const int32_t* cand = nullptr;      // [m][ef1] stage-① candidate ids (−1 padded)
+    const int32_t* sub_ell = nullptr;   // subgraph ELL
+    int32_t sub_w = 32;
+    const int32_t* full_ell = nullptr;  // full graph ELL
+    int32_t full_w = 32;
+    const float* xhat = nullptr;        // [n][xstride] X̂
+    int32_t xstride = 0;
+    int32_t hash_log2 = 12;
+    uint64_t* spill = nullptr;
+    int32_t spill_log2 = 16;
+    int32_t* work = nullptr;
+    int32_t* out_ids = nullptr;         // [m][k] full-space top-k
+    float* out_d = nullptr;
+    int32_t* counters = nullptr;        // [m][4] n_dist2, n_dist3, 0, status
+};
+int launch_refine(const DevIndex& ix, const Refine23& a, int grid_warps, cudaStream_t s);
+int refine_max_warps(const DevIndex& ix, const Refine23& a);
 
 // kernels (each returns the number of kernel launches it enqueued)
 int launch_project(const DevIndex& ix, const SearchArgs& a, cudaStream_t s);

@@ -128,16 +128,18 @@ struct pa_index {
     const float* h_rotated = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;                 // a7 handoff (D2H of candidates)
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // project | fes | traverse | refine
     std::vector<cudaEvent_t> pipe_done, pipe_copied;    // per sub-batch (stages ②③ pipeline)
     cudaEvent_t pipe_start = nullptr, pipe_end = nullptr;
     std::mutex mu;
     pa_stats stats{};
     bool events_pending = false;
+    bool last_full_gpu = false;           // last search ran ②③ on the GPU (counters2 valid)
     // workspace
     int64_t ws_m = 0;
     int32_t ws_E = 0, ws_ef = 0, ws_k = 0;
     float *q = nullptr, *qp = nullptr, *qres = nullptr, *cand_d = nullptr, *out_d = nullptr;
+    int32_t* counters2 = nullptr;          // [m][4] stages ②③ on the GPU: n_dist2, n_dist3, 0, status
     int32_t *cell = nullptr, *entries = nullptr, *cand_ids = nullptr, *out_ids = nullptr, *counters = nullptr,
             *work = nullptr, *perm = nullptr, *qoff = nullptr, *toff = nullptr;
     float* fes_scores = nullptr;
@@ -164,7 +166,9 @@ void free_ws(pa_index* ix) {
     cudaFree(ix->cell); cudaFree(ix->entries); cudaFree(ix->cand_ids); cudaFree(ix->out_ids);
     cudaFree(ix->counters); cudaFree(ix->work); cudaFree(ix->perm); cudaFree(ix->qoff); cudaFree(ix->toff);
     cudaFree(ix->fes_scores);
+    cudaFree(ix->counters2);
     ix->fes_scores = nullptr;
+    ix->counters2 = nullptr;
     ix->q = ix->qp = ix->qres = ix->cand_d = ix->out_d = nullptr;
     ix->cell = ix->entries = ix->cand_ids = ix->out_ids = ix->counters = ix->work = nullptr;
     ix->perm = ix->qoff = ix->toff = nullptr;
@@ -187,6 +191,7 @@ pa_status ensure_ws(pa_index* ix, int64_t m, int32_t E, int32_t ef, int32_t k) {
     CU(dalloc(&ix->out_ids, (size_t)m * k));
     CU(dalloc(&ix->out_d, (size_t)m * k));
     CU(dalloc(&ix->counters, (size_t)m * 4));
+    CU(dalloc(&ix->counters2, (size_t)m * 4));
     CU(dalloc(&ix->work, 4));
     CU(dalloc(&ix->perm, (size_t)m));
     CU(dalloc(&ix->qoff, (size_t)d.fes_r + 1));
@@ -218,7 +223,8 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, i
     pa_search_opts z{};
     if (!o) o = &z;
     r->stages = o->stages ? o->stages : PA_STAGES_GPU;
-    if (r->stages != PA_STAGES_GPU && r->stages != PA_STAGES_FULL) return fail(PA_EINVAL, "bad stages %d", r->stages);
+    if (r->stages != PA_STAGES_GPU && r->stages != PA_STAGES_FULL && r->stages != PA_STAGES_FULL_GPU)
+        return fail(PA_EINVAL, "bad stages %d", r->stages);
     if (k < 1) return fail(PA_EINVAL, "k = %d < 1", k);
     if (ef < k) return fail(PA_EINVAL, "ef = %d < k = %d", ef, k);
     r->ef1 = o->ef1 ? o->ef1 : ef;
@@ -236,9 +242,49 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, i
     if (r->ef1 > 256 || r->ef2 > 256 || r->ef3 > 256) return fail(PA_EINVAL, "ef > 256");
     if (r->ef1 < 1 || r->ef2 < 1 || r->ef3 < 1 || r->E < 1 || r->E > 1024) return fail(PA_EINVAL, "bad ef/entries");
     if (r->stages == PA_STAGES_GPU && k > r->ef1) return fail(PA_EINVAL, "k = %d > ef1 = %d", k, r->ef1);
-    if (r->stages == PA_STAGES_FULL && (k > r->ef3 || k > r->ef2)) return fail(PA_EINVAL, "k > ef2/ef3");
+    if (r->stages != PA_STAGES_GPU && (k > r->ef3 || k > r->ef2)) return fail(PA_EINVAL, "k > ef2/ef3");
     if (r->width != 1) return fail(PA_ENOTSUP, "search width w = %d: only w = 1 on the GPU", r->width);
     if (r->hash_log2 < 5 || r->hash_log2 > 15) return fail(PA_EINVAL, "hash_slots_log2 = %d", r->hash_log2);
+    return PA_OK;
+}
+
+// NEXT-f3: device copies of the full graph (ELL, −1 padded) and of X̂ (rows on a
+// 128-B-aligned stride) from the arrays pa_attach_host borrowed; once per index.
+pa_status ensure_full_device(pa_index* ix) {
+    auto& d = ix->dev;
+    if (d.xhat) return PA_OK;
+    if (!ix->h_rotated || !ix->h_full_off) return fail(PA_ESTATE, "PA_STAGES_FULL_GPU requires pa_attach_host");
+    const int64_t n = d.n;
+    int64_t maxdeg = 0;
+    for (int64_t u = 0; u < n; ++u) maxdeg = std::max<int64_t>(maxdeg, ix->h_full_off[u + 1] - ix->h_full_off[u]);
+    if (maxdeg > 64) return fail(PA_ENOTSUP, "PA_STAGES_FULL_GPU: full-graph degree %lld > 64", (long long)maxdeg);
+    const int w = maxdeg <= 32 ? 32 : 64;
+    const int xs = (d.dim + 31) & ~31;
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = (size_t)n * (w * 4 + (size_t)xs * 4);
+    if (need + ((size_t)1 << 30) > fr) return fail(PA_ENOMEM, "PA_STAGES_FULL_GPU: %zu MB needed, %zu MB free", need >> 20, fr >> 20);
+    int32_t* ell = nullptr;
+    float* xh = nullptr;
+    CU(dalloc(&ell, (size_t)n * w));
+    if (dalloc(&xh, (size_t)n * xs) != cudaSuccess) { cudaFree(ell); return fail(PA_ENOMEM, "X̂ allocation"); }
+    const int64_t chunk = 1 << 20;
+    std::vector<int32_t> eb((size_t)std::min(chunk, n) * w);
+    std::vector<float> xb((size_t)std::min(chunk, n) * xs);
+    for (int64_t s0 = 0; s0 < n; s0 += chunk) {
+        const int64_t s1 = std::min(n, s0 + chunk);
+        parallel_rows(s1 - s0, [&](int64_t lo, int64_t hi) {
+            for (int64_t i = lo; i < hi; ++i) {
+                const int64_t u = s0 + i, a0 = ix->h_full_off[u], a1 = ix->h_full_off[u + 1];
+                for (int j = 0; j < w; ++j) eb[(size_t)i * w + j] = a0 + j < a1 ? ix->h_full_nb[a0 + j] : -1;
+                std::memcpy(&xb[(size_t)i * xs], ix->h_rotated + u * d.dim, sizeof(float) * d.dim);
+                for (int j = d.dim; j < xs; ++j) xb[(size_t)i * xs + j] = 0.f;
+            }
+        });
+        CU(cudaMemcpy(ell + s0 * w, eb.data(), sizeof(int32_t) * (s1 - s0) * w, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(xh + s0 * xs, xb.data(), sizeof(float) * (s1 - s0) * xs, cudaMemcpyHostToDevice));
+    }
+    d.full_ell = ell; d.full_w = w; d.xhat = xh; d.xstride = xs;
     return PA_OK;
 }
 
@@ -303,7 +349,28 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     launches += pa::launch_traverse(ix->dev, a, (int)gridw, s);
     CU(cudaGetLastError());
     CU(cudaEventRecord(ix->ev[3], s));
+    if (r.stages == PA_STAGES_FULL_GPU) {                   // NEXT-f3: ②③ on the GPU
+        pa::Refine23 f;
+        f.m = m; f.k = k; f.ef1 = r.ef1; f.ef2 = r.ef2; f.ef3 = r.ef3; f.refine_iters = r.refine; f.flags = r.flags;
+        f.D = dd.dim; f.dp = dd.rdim; f.qlen = (dd.dim + 3) & ~3; f.qp = a.qp; f.qp_stride = dd.rdim_pad;
+        f.qres = a.qres; f.cand = a.cand_ids;
+        f.sub_ell = dd.ell; f.sub_w = dd.ell_w; f.full_ell = dd.full_ell; f.full_w = dd.full_w;
+        f.xhat = dd.xhat; f.xstride = dd.xstride;
+        f.hash_log2 = default_hash_log2(std::max(r.ef2, r.ef3), dd.n);
+        f.work = ix->work; f.out_ids = d_out_ids; f.out_d = d_out_d;
+        f.counters = ix->counters2 ? ix->counters2 + row0 * 4 : nullptr;
+        const int fw = pa::refine_max_warps(ix->dev, f);
+        if (fw <= 0) return fail(PA_ENOTSUP, "stage 2-3 kernel does not fit on an SM");
+        const int64_t fgw = std::min<int64_t>(fw, ((m + 3) / 4) * 4);
+        st = ensure_spill(ix, fgw);
+        if (st != PA_OK) return st;
+        f.spill = ix->spill; f.spill_log2 = ix->spill_log2;
+        launches += pa::launch_refine(ix->dev, f, (int)fgw, s);
+        CU(cudaGetLastError());
+    }
+    CU(cudaEventRecord(ix->ev[4], s));
     ix->events_pending = true;
+    ix->last_full_gpu = r.stages == PA_STAGES_FULL_GPU;
     ix->stats = pa_stats{};
     ix->stats.queries = m;
     ix->stats.kernel_launches = launches;
@@ -312,13 +379,15 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
 
 void collect_event_times(pa_index* ix) {
     if (!ix->events_pending) return;
-    cudaEventSynchronize(ix->ev[3]);
-    float t01 = 0, t12 = 0, t23 = 0, t03 = 0;
+    cudaEventSynchronize(ix->ev[4]);
+    float t01 = 0, t12 = 0, t23 = 0, t34 = 0, t04 = 0;
     cudaEventElapsedTime(&t01, ix->ev[0], ix->ev[1]);
     cudaEventElapsedTime(&t12, ix->ev[1], ix->ev[2]);
     cudaEventElapsedTime(&t23, ix->ev[2], ix->ev[3]);
-    cudaEventElapsedTime(&t03, ix->ev[0], ix->ev[3]);
-    ix->stats.ms_project = t01; ix->stats.ms_fes = t12; ix->stats.ms_traverse = t23; ix->stats.ms_total_gpu = t03;
+    cudaEventElapsedTime(&t34, ix->ev[3], ix->ev[4]);
+    cudaEventElapsedTime(&t04, ix->ev[0], ix->ev[4]);
+    ix->stats.ms_project = t01; ix->stats.ms_fes = t12; ix->stats.ms_traverse = t23; ix->stats.ms_refine = t34;
+    ix->stats.ms_total_gpu = t04;
     ix->events_pending = false;
 }
 
@@ -665,12 +734,16 @@ pa_status pa_search_device(pa_index* ix, const float* d_queries, int64_t m, int3
     Resolved r;
     pa_status st = resolve(opts, k, ef, &r, ix->dev.n);
     if (st != PA_OK) return st;
-    if (r.stages != PA_STAGES_GPU) return fail(PA_EINVAL, "pa_search_device runs stage 1 only");
+    if (r.stages == PA_STAGES_FULL) return fail(PA_EINVAL, "pa_search_device runs on the GPU only (stages 1 or 7)");
     std::lock_guard<std::mutex> g(ix->mu);
     CU(cudaSetDevice(ix->device));
     cudaStream_t s = (cudaStream_t)stream;          // NULL = the legacy default stream (CUDA convention)
     if (m == 0) return PA_OK;
-    return enqueue_gpu_stage(ix, d_queries, m, k, r, d_out_ids, d_out_dists, dbg, false, s);
+    if (r.stages == PA_STAGES_FULL_GPU) {
+        st = ensure_full_device(ix);
+        if (st != PA_OK) return st;
+    }
+    return enqueue_gpu_stage(ix, d_queries, m, k, r, d_out_ids, d_out_dists, dbg, r.stages == PA_STAGES_FULL_GPU, s);
 }
 
 static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m, int32_t k, const Resolved& r,
@@ -681,6 +754,10 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
     const bool full = !candidates_only && r.stages == PA_STAGES_FULL;
     if (full && (!ix->h_rotated || !ix->h_full_off))
         return fail(PA_ESTATE, "PA_STAGES_FULL requires pa_attach_host");
+    if (!candidates_only && r.stages == PA_STAGES_FULL_GPU) {
+        pa_status st0 = ensure_full_device(ix);
+        if (st0 != PA_OK) return st0;
+    }
     pa_status st = ensure_ws(ix, m, r.E, r.ef1, k);
     if (st != PA_OK) return st;
     const auto& d = ix->dev;
@@ -694,7 +771,8 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
     }
     const int64_t m0 = std::min(m, bsz);
     CU(cudaMemcpyAsync(ix->q, queries, sizeof(float) * m0 * d.dim, cudaMemcpyHostToDevice, s));
-    st = enqueue_gpu_stage(ix, ix->q, m0, k, r, ix->out_ids, ix->out_d, nullptr, full, s);
+    st = enqueue_gpu_stage(ix, ix->q, m0, k, r, ix->out_ids, ix->out_d, nullptr,
+                           full || r.stages == PA_STAGES_FULL_GPU, s);
     if (st != PA_OK) return st;
     int64_t launches = ix->stats.kernel_launches;
     if (candidates_only) {
@@ -834,6 +912,14 @@ pa_status pa_get_stats(const pa_index* cix, pa_stats* out, size_t size) {
             }
             ix->stats.sum_n_exp = se; ix->stats.sum_n_dist = sd; ix->stats.sum_spill = ss; ix->stats.overflow_queries = ov;
         }
+        if (ix->last_full_gpu && ix->counters2 &&
+            cudaMemcpy(c.data(), ix->counters2, sizeof(int32_t) * c.size(), cudaMemcpyDeviceToHost) == cudaSuccess) {
+            int64_t s2 = 0, s3 = 0, ov = 0;
+            for (int64_t q = 0; q < ix->stats.queries; ++q) {
+                s2 += c[q * 4]; s3 += c[q * 4 + 1]; ov += c[q * 4 + 3] != 0;
+            }
+            ix->stats.sum_n_dist2 = s2; ix->stats.sum_n_dist3 = s3; ix->stats.overflow_queries += ov;
+        }
     }
     std::memcpy(out, &ix->stats, sizeof(pa_stats));
     return PA_OK;
@@ -855,7 +941,7 @@ void pa_destroy(pa_index* ix) {
     auto& d = ix->dev;
     cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.reduced_h); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
     cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
-    cudaFree(d.pool_img); cudaFree(d.chunk_off);
+    cudaFree(d.pool_img); cudaFree(d.chunk_off); cudaFree(d.full_ell); cudaFree(d.xhat);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
     for (auto e : ix->pipe_done) cudaEventDestroy(e);
     for (auto e : ix->pipe_copied) cudaEventDestroy(e);

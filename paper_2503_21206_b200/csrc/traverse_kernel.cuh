@@ -24,6 +24,7 @@
 //              place (registers hold the old C across one __syncwarp).
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -605,6 +606,137 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
             }
             if (TRACE) { a.trace_nexp[q] = n_exp; a.trace_nvis[q] = n_dist; }
         }
+        __syncwarp();
+    }
+}
+
+}  // namespace trav
+}  // namespace pa
+
+namespace pa {
+namespace trav {
+
+// ---------------------------------------------------------------------------
+// NEXT-f3: stages ② and ③ on the GPU when the rotated full vectors X̂ fit in
+// HBM (oracle O8-O9).  One warp per query, exact visited set (the
+// compact/wide smem hash + global spill of the stage-① exact kernel):
+//   ② C := the stage-① candidates with full δ (all visited, the ef2 best kept,
+//      Q8 resize semantics), then `refine_iters` Alg 1 expansions on the
+//      SUBGRAPH with full δ;
+//   ③ every entry of C unchecked again, capacity ef3, Alg 1 on the FULL graph
+//      with full δ until no unchecked node, the visited set carried over (Q23).
+// PA_NO_STAGE2 skips ②'s expansions and keeps ef3 entries.  Rows of X̂ are
+// gathered 8 lanes per row (128-B segments; D = 96 rows are 384 B).
+template <int METRIC, int VIS, int SMAX, int NVR>
+__global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_refine(Refine23 a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int cap = max(a.ef2, a.ef3), S = 1 << a.hash_log2;
+    const int efp = (cap + 1) & ~1;
+    const int qlen = a.qlen;                                   // D rounded up to 4
+    const size_t per_warp = (size_t)efp * 8 + (size_t)qlen * 4 + 128 + (size_t)S * (VIS == 1 ? 2 : 4);
+    unsigned char* base = smem_raw + per_warp * w;
+    uint64_t* C = reinterpret_cast<uint64_t*>(base);
+    float* qs = reinterpret_cast<float*>(C + efp);
+    int32_t* scr = reinterpret_cast<int32_t*>(qs + qlen);
+    int32_t* H = scr + 32;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int64_t gw = (int64_t)blockIdx.x * kTW + w;
+    Visited vs;
+    vs.H = H;
+    vs.log2S = a.hash_log2;
+    vs.G = reinterpret_cast<uint32_t*>(a.spill + ((int64_t)gw << a.spill_log2));
+    vs.log = vs.G + ((size_t)1 << a.spill_log2);
+    vs.gmask = (1u << a.spill_log2) - 1u;
+    const int cap1 = S >> 1, cap2 = (int)(vs.gmask >> 1);
+    const unsigned char* rows = reinterpret_cast<const unsigned char*>(a.xhat);
+    const int64_t stride = (int64_t)a.xstride * 4;
+    const int nvr = qlen >> 2;
+
+    for (;;) {
+        int64_t q = 0;
+        if (lane == 0) q = atomicAdd(a.work, 1);
+        q = __shfl_sync(kFull, (int)q, 0);
+        if (q >= a.m) break;
+        vs.count1 = 0;
+        vs.count2 = 0;
+        for (int i = lane; i < qlen; i += 32)                   // q̂ = [q', q_res] (rotated query, fp32)
+            qs[i] = i < a.dp ? a.qp[q * a.qp_stride + i] : (i < a.D ? a.qres[q * (a.D - a.dp) + (i - a.dp)] : 0.f);
+        int4* H4 = reinterpret_cast<int4*>(H);
+        for (int i = lane; i < (S >> (VIS == 1 ? 3 : 2)); i += 32) H4[i] = make_int4(-1, -1, -1, -1);
+        __syncwarp();
+        int csz = 0, hint = 0, status = 0, n2 = 0, n3 = 0;
+        int ef = (a.flags & 2u) ? a.ef3 : a.ef2;                // current capacity of C
+        int* nd = &n2;
+        auto step = [&](int32_t v, bool unconditional) {
+            const bool open1 = vs.count1 + 32 <= cap1;
+            if (!open1 && vs.count2 + 32 > cap2) { status = 1; return; }
+            bool l2 = false;
+            uint32_t slot = 0;
+            const bool isnew = v >= 0 && visit<VIS>(vs, v, open1, l2, slot);
+            const unsigned bl2 = __ballot_sync(kFull, l2);
+            if (l2) vs.log[vs.count2 + __popc(bl2 & lt_mask)] = slot;
+            const unsigned bal = __ballot_sync(kFull, isnew);
+            const int nnew = __popc(bal);
+            vs.count1 += nnew - __popc(bl2);
+            vs.count2 += __popc(bl2);
+            *nd += nnew;
+            (void)unconditional;
+            if (nnew == 0) return;
+            if (isnew) scr[__popc(bal & lt_mask)] = v;
+            __syncwarp();
+            const int32_t cid = lane < nnew ? scr[lane] : 0;
+            __syncwarp();
+            const float d = group_dists<METRIC, NVR, false, 8, true>(qs, rows, stride, nvr, cid, nnew, lane);
+            const uint64_t key = lane < nnew ? make_key(d, cid) : kKeyInf;
+            const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
+            const bool pass = key < thresh;
+            const unsigned pb = __ballot_sync(kFull, pass);
+            if (pb == 0) return;
+            int minr;
+            csz = rank_merge<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
+            hint = min(hint, minr);
+        };
+        auto expand = [&](const int32_t* ell, int ellw, int max_it) {
+            for (int it = 0; status == 0 && (max_it < 0 || it < max_it); ++it) {
+                int p = -1;
+                for (int t = hint >> 5; t * 32 < csz; ++t) {
+                    const int i = t * 32 + lane;
+                    const unsigned b = __ballot_sync(kFull, i < csz && !key_checked(C[i]));
+                    if (b) { p = t * 32 + __ffs(b) - 1; break; }
+                }
+                if (p < 0) break;                                // Alg 1 l.12
+                const int32_t u = key_id(C[p]);
+                __syncwarp();
+                if (lane == 0) C[p] |= 1ull;
+                hint = p + 1;
+                __syncwarp();
+                for (int c = 0; c < ellw && status == 0; c += 32) step(__ldg(ell + (int64_t)u * ellw + c + lane), false);
+                if (it >= kIterCap) status = 2;
+            }
+        };
+        // ---- ② C := candidates with full δ, all visited (O8)
+        for (int j0 = 0; j0 < a.ef1 && status == 0; j0 += 32) {
+            const int j = j0 + lane;
+            step(j < a.ef1 ? a.cand[q * a.ef1 + j] : -1, true);
+        }
+        if (!(a.flags & 2u) && a.refine_iters > 0) expand(a.sub_ell, a.sub_w, a.refine_iters);
+        // ---- ③ carry unchecked, capacity ef3, Alg 1 on the full graph (O9)
+        for (int i = lane; i < csz; i += 32) C[i] &= ~1ull;
+        __syncwarp();
+        ef = a.ef3;
+        if (csz > ef) csz = ef;
+        hint = 0;
+        nd = &n3;
+        expand(a.full_ell, a.full_w, -1);
+        const float inf = __int_as_float(0x7f800000);
+        for (int i = lane; i < a.k; i += 32) {
+            a.out_ids[q * a.k + i] = i < csz ? key_id(C[i]) : -1;
+            a.out_d[q * a.k + i] = i < csz ? key_dist(C[i]) : inf;
+        }
+        for (int i = lane; i < vs.count2; i += 32) vs.G[vs.log[i]] = 0u;
+        __syncwarp();
+        if (lane == 0 && a.counters) reinterpret_cast<int4*>(a.counters)[q] = make_int4(n2, n3, 0, status);
         __syncwarp();
     }
 }

@@ -363,3 +363,48 @@ def test_no_pipeline_toggle_is_result_identical(s1):
     b = ix.search(s1["queries"], k=cfg.k, ef=cfg.ef, stages=pa.PA_STAGES_FULL, flags=pa.PA_NO_PIPELINE)
     ix.close()
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ------------------------------------------------ NEXT-f3: stages ②③ on the GPU --
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("flags", [0, 2])
+def test_full_gpu_integer_fixture_bit_exact(metric, flags):
+    """PA_STAGES_FULL_GPU (O8-O9 in one kernel, exact visited sets) vs the oracle's
+    three stages: exact arithmetic ⇒ identical ids and distances, with and without
+    stage ② (PA_NO_STAGE2)."""
+    inst = integer_instance(seed=21, metric=metric, n=400)
+    ix = pa.Index.from_instance(inst)
+    ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
+    for ef in (8, 32):
+        ids, d = ix.search(inst["queries"], k=5, ef=ef, stages=pa.PA_STAGES_FULL_GPU, flags=flags)
+        r = orc.search(inst, k=5, ef=ef, stages=3, flags=flags)
+        assert np.array_equal(ids, r["ids"]), ef
+        assert np.array_equal(d.astype(np.float64), r["d"]), ef
+    ix.close()
+
+
+@pytest.mark.parametrize("cfg_name", ["C0", "S1", "S2"])
+@pytest.mark.parametrize("bloom", [0, 12])
+def test_full_gpu_parity(cfg_name, bloom, request):
+    """Full-space recall@10 within 0.002 of the oracle's three stages (same stage-①
+    visited-set mode) and returned distances = fp64 full δ; the host pipeline
+    (PA_STAGES_FULL) and the GPU one agree on the same ground truth."""
+    inst = request.getfixturevalue(cfg_name.lower())
+    cfg = inst["cfg"]
+    ix = pa.Index.from_instance(inst)
+    ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
+    ids, d = ix.search(inst["queries"], k=cfg.k, ef=cfg.ef, stages=pa.PA_STAGES_FULL_GPU, bloom_log2=bloom)
+    st = ix.stats()
+    hids, _ = ix.search(inst["queries"], k=cfg.k, ef=cfg.ef, stages=pa.PA_STAGES_FULL, bloom_log2=bloom)
+    ix.close()
+    assert st["overflow_queries"] == 0 and st["sum_n_dist3"] > 0
+    r = orc.search(inst, k=cfg.k, ef=cfg.ef, stages=3, bloom_log2=bloom or None)
+    gt = inst["gt_ids"][:, :cfg.k]
+    rg, ro, rh = orc.recall(ids, gt, cfg.k), orc.recall(r["ids"], gt, cfg.k), orc.recall(hids, gt, cfg.k)
+    print(cfg_name, bloom, "full-gpu recall", rg, "oracle", ro, "host pipeline", rh)
+    assert abs(rg - ro) <= 0.002 + 1e-12 and abs(rg - rh) <= 0.002 + 1e-12
+    Qh = orc.project(inst["queries"], inst["basis"])
+    X = inst["rotated"].astype(np.float64)[ids]
+    want = ((X - Qh[:, None, :]) ** 2).sum(2) if cfg.metric == "l2" else -(X * Qh[:, None, :]).sum(2)
+    scale = np.abs(want) if cfg.metric == "l2" else np.abs(X * Qh[:, None, :]).sum(2)
+    assert np.all(np.abs(d - want) <= 1e-5 * scale + 1e-6 * np.sqrt(np.abs(want) * (Qh ** 2).sum(1, keepdims=True)))
