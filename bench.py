@@ -28,7 +28,7 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
-EF_SWEEP = (16, 24, 32, 48, 64, 96, 128, 192, 256)
+EF_SWEEP = (16, 24, 32, 40, 48, 56, 64, 72, 80, 88, 96, 112, 128, 160, 192, 224, 256)   # smallest ef reaching the target
 TARGET_RECALL = 0.90
 
 
