@@ -356,7 +356,7 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
         f.qres = a.qres; f.cand = a.cand_ids;
         f.sub_ell = dd.ell; f.sub_w = dd.ell_w; f.full_ell = dd.full_ell; f.full_w = dd.full_w;
         f.xhat = dd.xhat; f.xstride = dd.xstride;
-        f.hash_log2 = default_hash_log2(std::max(r.ef2, r.ef3), dd.n);
+        f.hash_log2 = dd.n <= (1 << 24) ? 12 : 11;        // ②③ visit ~20× ef ids: 8-KB smem table per query
         f.work = ix->work; f.out_ids = d_out_ids; f.out_d = d_out_d;
         f.counters = ix->counters2 ? ix->counters2 + row0 * 4 : nullptr;
         const int fw = pa::refine_max_warps(ix->dev, f);

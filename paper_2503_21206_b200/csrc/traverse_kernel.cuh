@@ -697,21 +697,42 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_refine(Refine23 a) {
             csz = rank_merge<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
             hint = min(hint, minr);
         };
+        // Alg 1 loop; the runner-up unchecked node's ELL row is loaded speculatively
+        // with the current one (it is the next expansion unless a new key beats it).
         auto expand = [&](const int32_t* ell, int ellw, int max_it) {
+            int32_t spec_u = -1, sv0 = -1, sv1 = -1;
             for (int it = 0; status == 0 && (max_it < 0 || it < max_it); ++it) {
-                int p = -1;
+                int p = -1, p2 = -1;
                 for (int t = hint >> 5; t * 32 < csz; ++t) {
                     const int i = t * 32 + lane;
                     const unsigned b = __ballot_sync(kFull, i < csz && !key_checked(C[i]));
-                    if (b) { p = t * 32 + __ffs(b) - 1; break; }
+                    if (b) {
+                        p = t * 32 + __ffs(b) - 1;
+                        const unsigned b2 = b & (b - 1);
+                        if (b2) p2 = t * 32 + __ffs(b2) - 1;
+                        break;
+                    }
                 }
                 if (p < 0) break;                                // Alg 1 l.12
                 const int32_t u = key_id(C[p]);
+                int32_t v0, v1 = -1;
+                if (u == spec_u) {
+                    v0 = sv0; v1 = sv1;
+                } else {
+                    v0 = __ldg(ell + (int64_t)u * ellw + lane);
+                    if (ellw > 32) v1 = __ldg(ell + (int64_t)u * ellw + 32 + lane);
+                }
+                spec_u = p2 >= 0 ? key_id(C[p2]) : -1;
+                if (spec_u >= 0) {
+                    sv0 = __ldg(ell + (int64_t)spec_u * ellw + lane);
+                    sv1 = ellw > 32 ? __ldg(ell + (int64_t)spec_u * ellw + 32 + lane) : -1;
+                }
                 __syncwarp();
                 if (lane == 0) C[p] |= 1ull;
                 hint = p + 1;
                 __syncwarp();
-                for (int c = 0; c < ellw && status == 0; c += 32) step(__ldg(ell + (int64_t)u * ellw + c + lane), false);
+                step(v0, false);
+                if (ellw > 32 && status == 0) step(v1, false);
                 if (it >= kIterCap) status = 2;
             }
         };
