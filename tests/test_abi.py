@@ -111,3 +111,31 @@ def test_validation_then_device(L, inst):
     with pytest.raises(pa.PAError) as e:
         _build(inst)
     assert e.value.status in (pa.PA_ECUDA, pa.PA_EINVAL)
+
+
+def test_binding_structs_match_the_header(tmp_path):
+    """The ctypes mirrors in the binding have the header's sizes and field
+    offsets (a C program compiled against include/pilotann.h prints them)."""
+    import subprocess
+    structs = {"pa_build_params": pa.BuildParams, "pa_search_opts": pa.SearchOpts, "pa_debug": pa.Debug,
+               "pa_stats": pa.Stats}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pilotann.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = subprocess.check_output([str(exe)], text=True).split("\n")
+    want = {}
+    for ln in out:
+        if ln:
+            a, b, c = ln.split()
+            want[(a, b)] = int(c)
+    for cname, py in structs.items():
+        assert C.sizeof(py) == want[(cname, "size")], cname
+        for f, _ in py._fields_:
+            assert getattr(py, f).offset == want[(cname, f)], (cname, f)
