@@ -534,13 +534,22 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
                 for (int it = 0;; ++it) {
                     if (TRACE && lane == 0 && n_exp < a.trace_cap) a.trace_expand[q * a.trace_cap + n_exp] = u;
                     ++n_exp;
+#ifndef PA_MERGE_FIRST
+#define PA_MERGE_FIRST 0
+#endif
+                    if (PA_MERGE_FIRST) {           // the merge overlaps the ELL-row load of u instead
+                        merge_keys(pkey, ppass, ppb);
+                        ppb = 0;
+                    }
                     // 1. visit u's neighbours, prefetch the new rows into L2
                     const bool isnew = visit_batch(vv, false);
                     if (status != 0) break;
                     if (isnew) prefetch_row_l2(row_ptr(vv), row_bytes);
                     // 2. merge the previous expansion's keys; runner-up r; its row speculatively
-                    merge_keys(pkey, ppass, ppb);
-                    ppb = 0;
+                    if (!PA_MERGE_FIRST) {
+                        merge_keys(pkey, ppass, ppb);
+                        ppb = 0;
+                    }
                     int pr = -1;
                     for (int t = hint >> 5; t * 32 < csz; ++t) {
                         const int i = t * 32 + lane;
@@ -548,7 +557,10 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
                         if (b) { pr = t * 32 + __ffs(b) - 1; break; }
                     }
                     const uint64_t key_r = pr >= 0 ? C[pr] : kKeyInf;
-                    if (pr >= 0 && key_id(key_r) != spec_u) {
+#ifndef PA_SPEC
+#define PA_SPEC 1
+#endif
+                    if (PA_SPEC && pr >= 0 && key_id(key_r) != spec_u) {
                         spec_u = key_id(key_r);
                         sv = __ldg(ix.ell + (int64_t)spec_u * 32 + lane);
                     }
