@@ -544,7 +544,10 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
                     // 1. visit u's neighbours, prefetch the new rows into L2
                     const bool isnew = visit_batch(vv, false);
                     if (status != 0) break;
-                    if (isnew) prefetch_row_l2(row_ptr(vv), row_bytes);
+#ifndef PA_ROWPF
+#define PA_ROWPF 0                      // L2 bulk prefetch of the new rows: A/B on C1 2.5% slower
+#endif
+                    if (PA_ROWPF && isnew) prefetch_row_l2(row_ptr(vv), row_bytes);
                     // 2. merge the previous expansion's keys; runner-up r; its row speculatively
                     if (!PA_MERGE_FIRST) {
                         merge_keys(pkey, ppass, ppb);
@@ -639,6 +642,9 @@ namespace trav {
 //      with full δ until no unchecked node, the visited set carried over (Q23).
 // PA_NO_STAGE2 skips ②'s expansions and keeps ef3 entries.  Rows of X̂ are
 // gathered 8 lanes per row (128-B segments; D = 96 rows are 384 B).
+#ifndef PA_REFINE_L
+#define PA_REFINE_L 8                  // lanes per X̂ row in the stage ②③ gathers
+#endif
 template <int METRIC, int VIS, int SMAX, int NVR>
 __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_refine(Refine23 a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -699,7 +705,7 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_refine(Refine23 a) {
             __syncwarp();
             const int32_t cid = lane < nnew ? scr[lane] : 0;
             __syncwarp();
-            const float d = group_dists<METRIC, NVR, false, 8, true>(qs, rows, stride, nvr, cid, nnew, lane);
+            const float d = group_dists<METRIC, NVR, false, PA_REFINE_L, true>(qs, rows, stride, nvr, cid, nnew, lane);
             const uint64_t key = lane < nnew ? make_key(d, cid) : kKeyInf;
             const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
             const bool pass = key < thresh;
