@@ -643,10 +643,13 @@ namespace trav {
 // PA_NO_STAGE2 skips ②'s expansions and keeps ef3 entries.  Rows of X̂ are
 // gathered 8 lanes per row (128-B segments; D = 96 rows are 384 B).
 #ifndef PA_REFINE_L
-#define PA_REFINE_L 8                  // lanes per X̂ row in the stage ②③ gathers
+#define PA_REFINE_L 4                  // lanes per X̂ row in the stage ②③ gathers (A/B: 8 is 8% slower)
 #endif
 template <int METRIC, int VIS, int SMAX, int NVR>
-__global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_refine(Refine23 a) {
+#ifndef PA_REFINE_MINB
+#define PA_REFINE_MINB 6
+#endif
+__global__ void __launch_bounds__(kTW * 32, PA_REFINE_MINB) k_refine(Refine23 a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int cap = max(a.ef2, a.ef3), S = 1 << a.hash_log2;
