@@ -587,6 +587,7 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
                     if (nxt == key_r) {
                         __syncwarp();
                         if (lane == 0) C[pr] = key_r | 1ull;
+                        __syncwarp();                         // visible before the next merge reads C
                         hint = pr + 1;
                     } else {
                         hint = pr >= 0 ? pr : csz;
