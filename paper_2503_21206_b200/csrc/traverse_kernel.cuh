@@ -571,6 +571,10 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
                     const uint64_t key = new_keys(vv, isnew);
                     const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
                     bool pass = key < thresh;
+#ifndef PA_ELLPF
+#define PA_ELLPF 0                      // L2 prefetch of passing keys' ELL rows: A/B on C1 3% slower
+#endif
+                    if (PA_ELLPF && pass) prefetch_row_l2(ix.ell + (int64_t)key_id(key) * 32, 128);
                     const unsigned pb = __ballot_sync(kFull, pass);
                     uint64_t nstar = kKeyInf;
                     if (pb) {
