@@ -408,3 +408,38 @@ def test_full_gpu_parity(cfg_name, bloom, request):
     want = ((X - Qh[:, None, :]) ** 2).sum(2) if cfg.metric == "l2" else -(X * Qh[:, None, :]).sum(2)
     scale = np.abs(want) if cfg.metric == "l2" else np.abs(X * Qh[:, None, :]).sum(2)
     assert np.all(np.abs(d - want) <= 1e-5 * scale + 1e-6 * np.sqrt(np.abs(want) * (Qh ** 2).sum(1, keepdims=True)))
+
+
+# ------------------------------------ the timed kernels = the traced kernels --
+# Trace outputs come from the runtime-row-length build of k_traverse_pipe; bench.py
+# times the compile-time-row-length builds (d' = 32/48/64/96/128).  Both must give
+# identical outputs, so the element-by-element oracle parity of the traced kernel
+# carries over to the timed one.
+@pytest.mark.parametrize("cfg_name", ["C0", "S1", "S2"])
+@pytest.mark.parametrize("bloom,fp16", [(0, False), (12, False), (12, True)])
+def test_timed_kernel_equals_traced_kernel(cfg_name, bloom, fp16, request):
+    inst = request.getfixturevalue(cfg_name.lower())
+    cfg = inst["cfg"]
+    ix = pa.Index.from_instance(inst, reduced_fp16=fp16)
+    for ef in (cfg.ef, 80):
+        traced = run_gpu(ix, inst, cfg.k, ef, trace_cap=8192, bloom_log2=bloom)
+        timed = run_gpu(ix, inst, cfg.k, ef, bloom_log2=bloom)
+        for key in ("ids", "d", "cand_ids", "cand_dists", "counters", "entries"):
+            assert np.array_equal(traced[key], timed[key]), (key, ef)
+    ix.close()
+
+
+@pytest.mark.parametrize("m", [1, 127, 128, 129, 300])
+def test_query_count_tails(m, s1):
+    """Batch sizes around the 128-row tcgen05 tiles (projection and per-cell FES
+    tiles): tie-aware parity with the oracle at every m."""
+    cfg = s1["cfg"]
+    rng = np.random.default_rng(m)
+    Q = s1["queries"][rng.integers(0, s1["queries"].shape[0], size=m)] + \
+        rng.normal(0, 0.01, size=(m, s1["D"])).astype(np.float32)
+    sub = dict(s1, queries=np.ascontiguousarray(Q, np.float32))
+    for bloom in (0, 12):
+        g, r = _both(sub, cfg.k, cfg.ef, trace_cap=8192, bloom_log2=bloom)
+        rep = compare(sub, g, r, cfg.k, cfg.ef)
+        assert not rep.fail, rep.fail[:3]
+        assert rep.exact >= 0.9 * m - 1
