@@ -443,3 +443,20 @@ def test_query_count_tails(m, s1):
         rep = compare(sub, g, r, cfg.k, cfg.ef)
         assert not rep.fail, rep.fail[:3]
         assert rep.exact >= 0.9 * m - 1
+
+
+@pytest.mark.parametrize("D,dp", [(128, 96), (160, 128), (64, 32)])
+@pytest.mark.parametrize("bloom", [0, 12])
+def test_row_length_specialisations(D, dp, bloom):
+    """The d' = 32/96/128 builds (bench configs C0, f2 d' = D = 96, C3S): oracle
+    parity of the traced kernel and identical outputs from the timed one."""
+    inst = tiny_instance(n=3000, D=D, dp=dp, R=16, m=96, seed=D + dp, member_ratio=0.6, r=8)
+    g, r = _both(inst, 10, 48, trace_cap=8192, bloom_log2=bloom)
+    rep = compare(inst, g, r, 10, 48)
+    assert not rep.fail, rep.fail[:3]
+    assert rep.exact >= 0.9 * 96
+    ix = pa.Index.from_instance(inst)
+    timed = run_gpu(ix, inst, 10, 48, bloom_log2=bloom)
+    ix.close()
+    for key in ("ids", "d", "cand_ids", "cand_dists", "counters"):
+        assert np.array_equal(g[key], timed[key]), key
