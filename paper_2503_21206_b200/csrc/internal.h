@@ -46,7 +46,6 @@ struct SearchArgs {
     uint32_t flags = 0;
     int32_t hash_log2 = 12;
     int32_t bloom_log2 = 0;        // > 0: stage-① visited set = bloom filter, 3 segments × 2^this bits (NEXT-f1)
-    int32_t ef_init = 0;           // > 0: capacity of C while the entries are inserted (stage ③ on the GPU: ef2)
     const float* q = nullptr;      // [m][dim]
     float* qp = nullptr;           // [m][rdim_pad]  projected q'
     float* qres = nullptr;         // [m][dim − rdim] (optional) residual projection for host stages
@@ -97,8 +96,6 @@ struct Refine23 {
     int32_t* out_ids = nullptr;         // [m][k] full-space top-k
     float* out_d = nullptr;
     int32_t* counters = nullptr;        // [m][4] n_dist2, n_dist3, 0, status
-    int32_t* vis_out = nullptr;         // if set: stop after ② and write its visited ids [m][vis_cap] (−1 padded)
-    int32_t vis_cap = 0;
 };
 int launch_refine(const DevIndex& ix, const Refine23& a, int grid_warps, cudaStream_t s);
 int refine_max_warps(const DevIndex& ix, const Refine23& a);

@@ -135,12 +135,6 @@ struct pa_index {
     pa_stats stats{};
     bool events_pending = false;
     bool last_full_gpu = false;           // last search ran ②③ on the GPU (counters2 valid)
-    bool last_pipe3 = false;              // ... with stage ③ in the pipelined traversal (counters3 valid)
-    int32_t* vis2 = nullptr;              // [m][vis2_cap] stage-② visited ids handed to stage ③
-    float* qfull = nullptr;               // [m][D] rotated queries q̂ for stage ③
-    int32_t* counters3 = nullptr;         // [m][4] stage-③ traversal counters
-    int64_t s3_m = 0;
-    int32_t s3_cap = 0;
     // workspace
     int64_t ws_m = 0;
     int32_t ws_E = 0, ws_ef = 0, ws_k = 0;
@@ -251,19 +245,6 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, i
     if (r->stages != PA_STAGES_GPU && (k > r->ef3 || k > r->ef2)) return fail(PA_EINVAL, "k > ef2/ef3");
     if (r->width != 1) return fail(PA_ENOTSUP, "search width w = %d: only w = 1 on the GPU", r->width);
     if (r->hash_log2 < 5 || r->hash_log2 > 15) return fail(PA_EINVAL, "hash_slots_log2 = %d", r->hash_log2);
-    return PA_OK;
-}
-
-pa_status ensure_stage3_ws(pa_index* ix, int64_t m, int32_t vcap) {
-    if (m <= ix->s3_m && vcap <= ix->s3_cap) return PA_OK;
-    cudaFree(ix->vis2); cudaFree(ix->qfull); cudaFree(ix->counters3);
-    ix->vis2 = nullptr; ix->qfull = nullptr; ix->counters3 = nullptr; ix->s3_m = 0;
-    m = std::max<int64_t>(m, ix->ws_m);
-    vcap = std::max(vcap, ix->s3_cap);
-    CU(dalloc(&ix->vis2, (size_t)m * vcap));
-    CU(dalloc(&ix->qfull, (size_t)m * ix->dev.dim));
-    CU(dalloc(&ix->counters3, (size_t)m * 4));
-    ix->s3_m = m; ix->s3_cap = vcap;
     return PA_OK;
 }
 
@@ -384,48 +365,8 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
         st = ensure_spill(ix, fgw);
         if (st != PA_OK) return st;
         f.spill = ix->spill; f.spill_log2 = ix->spill_log2;
-        // Stage ③ through the pipelined traversal when the full graph fits its ELL-32
-        // layout: k_refine stops after ② and hands over its visited ids; the pipe
-        // kernel re-inserts them (C holds the best ef2 = C2, Q23) and runs Alg 1 on the
-        // full graph with X̂ rows.  PA_STAGE3=refine keeps the one-kernel path.
-        const char* s3e = std::getenv("PA_STAGE3");
-        const bool pipe3 = dd.full_w == 32 && (dd.dim % 4) == 0 && !(s3e && !std::strcmp(s3e, "refine"));
-        if (pipe3) {
-            const int vcap = r.ef1 + ((r.flags & PA_NO_STAGE2) ? 0 : r.refine * dd.ell_w);
-            st = ensure_stage3_ws(ix, row0 + m, vcap);
-            if (st != PA_OK) return st;
-            int32_t* vis = ix->vis2 + row0 * vcap;
-            float* qf = ix->qfull + row0 * dd.dim;
-            f.vis_out = vis; f.vis_cap = vcap;
-            launches += pa::launch_refine(ix->dev, f, (int)fgw, s);
-            CU(cudaGetLastError());
-            CU(cudaMemcpy2DAsync(qf, sizeof(float) * dd.dim, a.qp, sizeof(float) * dd.rdim_pad, sizeof(float) * dd.rdim,
-                                 m, cudaMemcpyDeviceToDevice, s));
-            if (dd.dim > dd.rdim)
-                CU(cudaMemcpy2DAsync(qf + dd.rdim, sizeof(float) * dd.dim, a.qres, sizeof(float) * (dd.dim - dd.rdim),
-                                     sizeof(float) * (dd.dim - dd.rdim), m, cudaMemcpyDeviceToDevice, s));
-            pa::DevIndex v3 = dd;
-            v3.ell = dd.full_ell; v3.ell_w = 32; v3.reduced = dd.xhat; v3.reduced_h = nullptr;
-            v3.rstride = dd.xstride; v3.rdim = dd.dim; v3.rdim_pad = dd.dim; v3.qlen = dd.dim;
-            pa::SearchArgs a3;
-            a3.m = m; a3.k = k; a3.ef = r.ef3; a3.ef_init = (r.flags & PA_NO_STAGE2) ? r.ef3 : r.ef2;
-            a3.E = vcap; a3.entries = vis; a3.flags = 0; a3.bloom_log2 = 0;
-            a3.hash_log2 = dd.n <= (1 << 24) ? 12 : 11;
-            a3.qp = qf; a3.out_ids = d_out_ids; a3.out_d = d_out_d;
-            a3.counters = ix->counters3 + row0 * 4; a3.work = ix->work;
-            const int w3 = pa::traverse_max_warps(v3, a3);
-            if (w3 <= 0) return fail(PA_ENOTSUP, "stage-3 traversal does not fit on an SM");
-            const int64_t g3 = std::min<int64_t>(w3, ((m + 3) / 4) * 4);
-            st = ensure_spill(ix, g3);
-            if (st != PA_OK) return st;
-            a3.spill = ix->spill; a3.spill_log2 = ix->spill_log2; a3.spill_warps = ix->spill_warps;
-            launches += pa::launch_traverse(v3, a3, (int)g3, s);
-            CU(cudaGetLastError());
-        } else {
-            launches += pa::launch_refine(ix->dev, f, (int)fgw, s);
-            CU(cudaGetLastError());
-        }
-        ix->last_pipe3 = pipe3;
+        launches += pa::launch_refine(ix->dev, f, (int)fgw, s);
+        CU(cudaGetLastError());
     }
     CU(cudaEventRecord(ix->ev[4], s));
     ix->events_pending = true;
@@ -977,11 +918,6 @@ pa_status pa_get_stats(const pa_index* cix, pa_stats* out, size_t size) {
             for (int64_t q = 0; q < ix->stats.queries; ++q) {
                 s2 += c[q * 4]; s3 += c[q * 4 + 1]; ov += c[q * 4 + 3] != 0;
             }
-            if (ix->last_pipe3 && ix->counters3 &&
-                cudaMemcpy(c.data(), ix->counters3, sizeof(int32_t) * c.size(), cudaMemcpyDeviceToHost) == cudaSuccess) {
-                s3 = 0;                                     // stage-③ distances (incl. the re-scored carry)
-                for (int64_t q = 0; q < ix->stats.queries; ++q) { s3 += c[q * 4 + 1]; ov += c[q * 4 + 3] != 0; }
-            }
             ix->stats.sum_n_dist2 = s2; ix->stats.sum_n_dist3 = s3; ix->stats.overflow_queries += ov;
         }
     }
@@ -1006,7 +942,6 @@ void pa_destroy(pa_index* ix) {
     cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.reduced_h); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
     cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
     cudaFree(d.pool_img); cudaFree(d.chunk_off); cudaFree(d.full_ell); cudaFree(d.xhat);
-    cudaFree(ix->vis2); cudaFree(ix->qfull); cudaFree(ix->counters3);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
     for (auto e : ix->pipe_done) cudaEventDestroy(e);
     for (auto e : ix->pipe_copied) cudaEventDestroy(e);

@@ -496,24 +496,22 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
             n_dist += nnew;
             return isnew;
         };
-        auto merge_keys = [&](uint64_t key, bool pass, unsigned pb, int cap) {
+        auto merge_keys = [&](uint64_t key, bool pass, unsigned pb) {
             if (pb == 0) return;
             int minr;
-            csz = rank_merge<SMAX>(C, csz, cap, key, pass, pb, lane, minr);
+            csz = rank_merge<SMAX>(C, csz, ef, key, pass, pb, lane, minr);
             hint = min(hint, minr);
         };
-        // ---- a5: C := entries, visited := entries (sequential merges); C holds at
-        // most ef_init of them when set (stage ③ on the GPU starts from C2, ef2 ≤ ef3)
-        const int ci = (a.ef_init > 0 && a.ef_init < ef) ? a.ef_init : ef;
+        // ---- a5: C := entries, visited := entries (sequential merges)
         for (int j0 = 0; j0 < a.E && status == 0; j0 += 32) {
             const int j = j0 + lane;
             const int32_t v = j < a.E ? a.entries[q * a.E + j] : -1;
             const bool isnew = visit_batch(v, true);
             if (status != 0) break;
             const uint64_t key = new_keys(v, isnew);
-            const uint64_t thresh = csz == ci ? C[ci - 1] : kKeyInf;
+            const uint64_t thresh = csz == ef ? C[ef - 1] : kKeyInf;
             const bool pass = key < thresh;
-            merge_keys(key, pass, __ballot_sync(kFull, pass), ci);
+            merge_keys(key, pass, __ballot_sync(kFull, pass));
         }
         // ---- a6: pipelined Alg 1 loop
         if (!(a.flags & 4u) && status == 0) {
@@ -540,7 +538,7 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
 #define PA_MERGE_FIRST 1                // A/B on C1: 2% faster than merging after the visit
 #endif
                     if (PA_MERGE_FIRST) {           // the merge overlaps the ELL-row load of u instead
-                        merge_keys(pkey, ppass, ppb, ef);
+                        merge_keys(pkey, ppass, ppb);
                         ppb = 0;
                     }
                     // 1. visit u's neighbours, prefetch the new rows into L2
@@ -552,7 +550,7 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
                     if (PA_ROWPF && isnew) prefetch_row_l2(row_ptr(vv), row_bytes);
                     // 2. merge the previous expansion's keys; runner-up r; its row speculatively
                     if (!PA_MERGE_FIRST) {
-                        merge_keys(pkey, ppass, ppb, ef);
+                        merge_keys(pkey, ppass, ppb);
                         ppb = 0;
                     }
                     int pr = -1;
@@ -604,7 +602,7 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
                     vv = (u == spec_u) ? sv : __ldg(ix.ell + (int64_t)u * 32 + lane);
                     if (it >= kIterCap) { status = 2; break; }
                 }
-                merge_keys(pkey, ppass, ppb, ef);    // pending keys (overflow / cap exits)
+                merge_keys(pkey, ppass, ppb);        // pending keys (overflow / cap exits)
             }
         }
         // ---- outputs
@@ -708,10 +706,6 @@ __global__ void __launch_bounds__(kTW * 32, PA_REFINE_MINB) k_refine(Refine23 a)
             const int nnew = __popc(bal);
             vs.count1 += nnew - __popc(bl2);
             vs.count2 += __popc(bl2);
-            if (a.vis_out && isnew) {
-                const int pos = *nd + __popc(bal & lt_mask);
-                if (pos < a.vis_cap) a.vis_out[q * a.vis_cap + pos] = v;
-            }
             *nd += nnew;
             (void)unconditional;
             if (nnew == 0) return;
@@ -774,14 +768,6 @@ __global__ void __launch_bounds__(kTW * 32, PA_REFINE_MINB) k_refine(Refine23 a)
             step(j < a.ef1 ? a.cand[q * a.ef1 + j] : -1, true);
         }
         if (!(a.flags & 2u) && a.refine_iters > 0) expand(a.sub_ell, a.sub_w, a.refine_iters);
-        if (a.vis_out) {                                        // ③ runs in k_traverse_pipe
-            for (int i = n2 + lane; i < a.vis_cap; i += 32) a.vis_out[q * a.vis_cap + i] = -1;
-            for (int i = lane; i < vs.count2; i += 32) vs.G[vs.log[i]] = 0u;
-            __syncwarp();
-            if (lane == 0 && a.counters) reinterpret_cast<int4*>(a.counters)[q] = make_int4(n2, 0, 0, status);
-            __syncwarp();
-            continue;
-        }
         // ---- ③ carry unchecked, capacity ef3, Alg 1 on the full graph (O9)
         for (int i = lane; i < csz; i += 32) C[i] &= ~1ull;
         __syncwarp();
