@@ -23,8 +23,10 @@
  *     PA_IP = negative inner product (−q·x), so smaller is better for both.
  *     Results are ordered by (distance, id) ascending (Q13); rows with fewer
  *     than k valid results are padded with id −1 and distance +inf (Q26).
- *   - One pa_search at a time per index (calls serialise on an internal
- *     mutex); separate indexes are independent.  One process per GPU is the
+ *   - One search at a time per index: calls serialise on an internal mutex,
+ *     and on the device every search (whatever stream it is enqueued on) waits
+ *     for the end of the previous one, because they share the index's device
+ *     workspace; separate indexes are independent.  One process per GPU is the
  *     intended multi-GPU layout: each process builds its own replica with
  *     params.device and searches its shard of the queries.
  * ========================================================================== */
@@ -95,6 +97,10 @@ typedef struct {
                                       rounded once (RNE) at build; stage ① and the FES pool then use
                                       exactly these rounded values (half the gather bytes); stage ②
                                       recomputes full δ from X̂.  0 = fp32 rows (default)            */
+    int64_t reduced_stride;        /* floats between consecutive rows of `reduced` (0 ⇒ rdim).  With
+                                      stride = dim the caller passes X̂ itself: x_primary is exactly the
+                                      first d' columns of X̂ = X·V, so a 100M-row index
+                                      needs no separate [n][d'] host copy.  Must be ≥ rdim (PA_EINVAL). */
 } pa_build_params;
 
 /* Per-call options; pass NULL for defaults.  Zero fields take defaults
@@ -175,7 +181,8 @@ pa_status pa_search_device(pa_index* ix, const float* d_queries, int64_t m, int3
                            const pa_debug* dbg, void* stream);
 
 /* Stage-① candidate lists for HOST queries: cand_ids/cand_dists [m][ef] (HOST),
- * i.e. what the GPU hands to the host stages ("<1KB per query"). */
+ * i.e. what the GPU hands to the host stages ("<1KB per query").
+ * opts->stages must be 0 or PA_STAGES_GPU (PA_EINVAL otherwise). */
 pa_status pa_search_candidates(pa_index* ix, const float* queries, int64_t m, int32_t ef,
                                const pa_search_opts* opts, int32_t* cand_ids, float* cand_dists);
 

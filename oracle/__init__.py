@@ -35,7 +35,8 @@ class OrcIndex(C.Structure):
                 ("sub_offsets", C.c_void_p), ("sub_neighbors", C.c_void_p), ("reduced", C.c_void_p),
                 ("basis", C.c_void_p), ("fes_r", C.c_int32), ("fes_centroids", C.c_void_p),
                 ("fes_cell_off", C.c_void_p), ("fes_pool_ids", C.c_void_p),
-                ("full_offsets", C.c_void_p), ("full_neighbors", C.c_void_p), ("rotated", C.c_void_p)]
+                ("full_offsets", C.c_void_p), ("full_neighbors", C.c_void_p), ("rotated", C.c_void_p),
+                ("reduced_stride", C.c_int64)]
 
 
 class OrcOpts(C.Structure):
@@ -88,11 +89,21 @@ def default_budgets(k: int, ef: int):
     return dict(ef1=ef, ef2=max(k, ef // 2), ef3=ef, entries=ef, width=1, refine_iters=2)
 
 
+def _rows(a):
+    """fp32 rows, possibly a column slice of a wider array (X̂[:, :d']) → (array, row stride)."""
+    a = np.asarray(a)
+    if a.ndim == 2 and a.dtype == np.float32 and a.strides[1] == 4 and a.strides[0] % 4 == 0:
+        return a, a.strides[0] // 4
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a, a.shape[1]
+
+
 def make_index(inst: dict):
     """Keep contiguous copies alive inside the returned tuple (index struct, arrays)."""
+    red, rstride = _rows(inst["reduced"])
     arrs = dict(
         sub_offsets=_c(inst["sub_offsets"], np.int64), sub_neighbors=_c(inst["sub_neighbors"], np.int32),
-        reduced=_c(inst["reduced"], np.float32), basis=_c(inst["basis"], np.float32),
+        reduced=red, basis=_c(inst["basis"], np.float32),
         fes_centroids=_c(inst["fes_centroids"], np.float32), fes_cell_off=_c(inst["fes_cell_off"], np.int64),
         fes_pool_ids=_c(inst["fes_pool_ids"], np.int32),
         full_offsets=_c(inst.get("full_offsets"), np.int64), full_neighbors=_c(inst.get("full_neighbors"), np.int32),
@@ -105,7 +116,7 @@ def make_index(inst: dict):
                   fes_r=int(arrs["fes_cell_off"].shape[0] - 1), fes_centroids=_p(arrs["fes_centroids"]),
                   fes_cell_off=_p(arrs["fes_cell_off"]), fes_pool_ids=_p(arrs["fes_pool_ids"]),
                   full_offsets=_p(arrs["full_offsets"]), full_neighbors=_p(arrs["full_neighbors"]),
-                  rotated=_p(arrs["rotated"]))
+                  rotated=_p(arrs["rotated"]), reduced_stride=rstride)
     return ix, arrs
 
 

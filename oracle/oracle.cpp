@@ -64,6 +64,7 @@ struct OrcIndex {
     const int64_t* full_offsets;    // [n+1]   full graph (stage ③); may be null
     const int32_t* full_neighbors;
     const float* rotated;           // [n][dim] X̂ = X·V (stages ②③); may be null
+    int64_t reduced_stride;         // floats between rows of `reduced` (0 ⇒ rdim; dim when it is X̂ itself)
 };
 
 struct OrcOpts {
@@ -207,7 +208,8 @@ void search_one(const OrcIndex& ix, const float* q, const OrcOpts& o, const OrcO
         qh[j] = s;
     }
     const double* qp = qh.data();                          // q' = q̂[0:d']
-    auto dprime = [&](int32_t v) { return delta(qp, ix.reduced + (int64_t)v * dp, dp, metric); };
+    const int64_t rs = ix.reduced_stride ? ix.reduced_stride : dp;
+    auto dprime = [&](int32_t v) { return delta(qp, ix.reduced + (int64_t)v * rs, dp, metric); };
     auto dfull = [&](int32_t v) { return delta(qh.data(), ix.rotated + (int64_t)v * D, D, metric); };
 
     // ---- O3 routing (Alg 2 l.8 "Q[i] not closest to block")

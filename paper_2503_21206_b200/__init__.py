@@ -45,7 +45,8 @@ class BuildParams(C.Structure):
                 ("metric", C.c_int32), ("sub_offsets", C.c_void_p), ("sub_neighbors", C.c_void_p),
                 ("member_flags", C.c_void_p), ("reduced", C.c_void_p), ("basis", C.c_void_p),
                 ("fes_r", C.c_int32), ("fes_centroids", C.c_void_p), ("fes_cell_off", C.c_void_p),
-                ("fes_pool_ids", C.c_void_p), ("device", C.c_int32), ("reduced_fp16", C.c_int32)]
+                ("fes_pool_ids", C.c_void_p), ("device", C.c_int32), ("reduced_fp16", C.c_int32),
+                ("reduced_stride", C.c_int64)]
 
 
 class SearchOpts(C.Structure):
@@ -124,6 +125,42 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
+def _rows(a):
+    """fp32 row-major rows, possibly a column slice of a wider array (e.g. the
+    first d' columns of X̂): → (array whose .ctypes.data is row 0, row stride in floats)."""
+    a = np.asarray(a)
+    if a.ndim == 2 and a.dtype == np.float32 and a.strides[1] == 4 and a.strides[0] % 4 == 0 \
+            and a.strides[0] >= 4 * a.shape[1]:
+        return a, a.strides[0] // 4
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a, a.shape[1] if a.ndim == 2 else 0
+
+
+def _host_rows(x, cols, dtype, name):
+    """A host [m][cols] array of `dtype` from numpy or a CPU torch tensor → (pointer, m, keep-alive)."""
+    if hasattr(x, "data_ptr"):
+        if x.device.type != "cpu":
+            raise ValueError(f"{name}: expected a CPU tensor (got {x.device}); use search_device for device buffers")
+        want = {np.float32: "torch.float32", np.int32: "torch.int32"}[dtype]
+        if str(x.dtype) != want or not x.is_contiguous() or x.dim() != 2 or (cols and x.shape[1] != cols):
+            raise ValueError(f"{name}: expected a contiguous {want} tensor [m][{cols}], got {tuple(x.shape)} {x.dtype}")
+        return x.data_ptr(), int(x.shape[0]), x
+    a = np.asarray(x)
+    if a.ndim != 2 or (cols and a.shape[1] != cols):
+        raise ValueError(f"{name}: expected [m][{cols}], got {a.shape}")
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return _ptr(a), a.shape[0], a
+
+
+def _dev_rows(x, rows, cols, dtype, device, name):
+    want = {np.float32: "torch.float32", np.int32: "torch.int32"}[dtype]
+    if x.device.type != "cuda" or x.device.index != device:
+        raise ValueError(f"{name}: expected a tensor on cuda:{device}, got {x.device}")
+    if str(x.dtype) != want or not x.is_contiguous() or x.dim() != 2 or x.shape[1] != cols \
+            or (rows is not None and x.shape[0] != rows):
+        raise ValueError(f"{name}: expected a contiguous {want} tensor [{rows}][{cols}], got {tuple(x.shape)} {x.dtype}")
+
+
 def make_opts(stages=PA_STAGES_GPU, ef1=0, ef2=0, ef3=0, entries=0, width=0, refine_iters=0, flags=0,
               hash_slots_log2=0, host_threads=0, bloom_log2=0) -> SearchOpts:
     return SearchOpts(stages=stages, ef1=ef1, ef2=ef2, ef3=ef3, entries=entries, width=width,
@@ -139,7 +176,7 @@ class Index:
                  reduced_fp16=False):
         so = _c(sub_offsets, np.int64)
         sn = _c(sub_neighbors, np.int32)
-        red = _c(reduced, np.float32)
+        red, rstride = _rows(reduced)
         bas = _c(basis, np.float32)
         cen = _c(fes_centroids, np.float32)
         coff = _c(fes_cell_off, np.int64)
@@ -154,7 +191,7 @@ class Index:
                         sub_offsets=_ptr(so), sub_neighbors=_ptr(sn), member_flags=_ptr(mf),
                         reduced=_ptr(red), basis=_ptr(bas), fes_r=int(coff.shape[0] - 1),
                         fes_centroids=_ptr(cen), fes_cell_off=_ptr(coff), fes_pool_ids=_ptr(pool),
-                        device=int(device), reduced_fp16=1 if reduced_fp16 else 0)
+                        device=int(device), reduced_fp16=1 if reduced_fp16 else 0, reduced_stride=int(rstride))
         h = C.c_void_p()
         _check(lib().pa_build(C.byref(p), C.byref(h)))
         self._h = h
@@ -180,31 +217,38 @@ class Index:
     def search(self, queries, k=10, ef=64, opts: SearchOpts | None = None, out=None, **kw):
         """pa_search on HOST buffers.  `queries`/`out` may be numpy arrays or
         (pinned) CPU torch tensors; results are written into `out`."""
-        if hasattr(queries, "data_ptr"):
-            qp, m = queries.data_ptr(), int(queries.shape[0])
-        else:
-            q = _c(queries, np.float32)
-            qp, m = _ptr(q), q.shape[0]
+        qp, m, _keep = _host_rows(queries, self.dim, np.float32, "queries")
         if out is None:
             out = (np.empty((m, k), np.int32), np.empty((m, k), np.float32))
-        op = [o.data_ptr() if hasattr(o, "data_ptr") else _ptr(o) for o in out]
+        op = []
+        for o_, dt, nm in zip(out, (np.int32, np.float32), ("out ids", "out dists")):
+            if not hasattr(o_, "data_ptr") and not (isinstance(o_, np.ndarray) and o_.flags.c_contiguous
+                                                    and o_.dtype == dt):
+                raise ValueError(f"{nm}: expected a C-contiguous {np.dtype(dt).name} array [m][k]")
+            p_, mo, _ = _host_rows(o_, k, dt, nm)
+            if mo != m:
+                raise ValueError(f"{nm}: {mo} rows for {m} queries")
+            op.append(p_)
         o = opts if opts is not None else make_opts(**kw)
         _check(lib().pa_search(self._h, qp, m, k, ef, C.byref(o), op[0], op[1]))
         return out
 
     def search_candidates(self, queries, ef=64, opts: SearchOpts | None = None, **kw):
-        q = _c(queries, np.float32)
-        m = q.shape[0]
+        qp, m, q = _host_rows(queries, self.dim, np.float32, "queries")
         ids = np.empty((m, ef), np.int32)
         d = np.empty((m, ef), np.float32)
         o = opts if opts is not None else make_opts(**kw)
-        _check(lib().pa_search_candidates(self._h, _ptr(q), m, ef, C.byref(o), _ptr(ids), _ptr(d)))
+        _check(lib().pa_search_candidates(self._h, qp, m, ef, C.byref(o), _ptr(ids), _ptr(d)))
         return ids, d
 
     # -- pa_search_device (torch CUDA tensors; pointers only) ----------------
     def search_device(self, q, k, ef, out_ids, out_d, opts: SearchOpts | None = None, debug: Debug | None = None,
                       stream=None, **kw):
         o = opts if opts is not None else make_opts(**kw)
+        _dev_rows(q, None, self.dim, np.float32, self.device, "queries")
+        m = int(q.shape[0])
+        _dev_rows(out_ids, m, k, np.int32, self.device, "out_ids")
+        _dev_rows(out_d, m, k, np.float32, self.device, "out_d")
         if stream is None:
             import torch
             stream = torch.cuda.current_stream(q.device).cuda_stream

@@ -170,6 +170,9 @@ void run_host_stages(const HostStageArgs& a) {
                 greedy(a.sub.off, a.sub.nb, dfull, pref, a.ef2, a.refine_iters, C, vis, my2);
             }
             // ---- stage ③: Alg 1 on the full graph, carry entries unchecked, visited kept (Q23)
+            // ef2 > ef3: keep the ef3 smallest now — the same set Alg 1's resize (l.11)
+            // leaves after the first expansion, whose node is C[0] either way.
+            if ((int)C.size() > a.ef3) C.resize(a.ef3);
             for (Cand& c : C) c.checked = false;
             greedy(a.full.off, a.full.nb, dfull, pref, a.ef3, -1, C, vis, my3);
             for (int j = 0; j < a.k; ++j) {

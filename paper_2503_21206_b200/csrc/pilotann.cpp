@@ -131,6 +131,8 @@ struct pa_index {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // project | fes | traverse | refine
     std::vector<cudaEvent_t> pipe_done, pipe_copied;    // per sub-batch (stages ②③ pipeline)
     cudaEvent_t pipe_start = nullptr, pipe_end = nullptr;
+    cudaEvent_t done_ev = nullptr;         // end of the last enqueued search (any stream)
+    bool done_recorded = false;
     std::mutex mu;
     pa_stats stats{};
     bool events_pending = false;
@@ -295,6 +297,12 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     pa_status st = ensure_ws(ix, row0 + m, r.E, r.ef1, k);
     if (st != PA_OK) return st;
     const auto& dd = ix->dev;
+    if (r.stages == PA_STAGES_FULL_GPU && (!dd.xhat || !dd.full_ell))
+        return fail(PA_ESTATE, "stages 2-3 on the GPU need the device copy of the full graph and X-hat");
+    // Every search on this index shares its workspace (work counter, candidate and
+    // spill buffers): a search enqueued on another stream first waits for the end
+    // of the previous one, so calls serialise on the device as well as on the mutex.
+    if (ix->done_recorded) CU(cudaStreamWaitEvent(s, ix->done_ev, 0));
     pa::SearchArgs a;
     a.m = m; a.k = k; a.ef = r.ef1; a.E = r.E; a.flags = r.flags; a.hash_log2 = r.hash_log2;
     a.bloom_log2 = r.bloom_log2;
@@ -369,6 +377,8 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
         CU(cudaGetLastError());
     }
     CU(cudaEventRecord(ix->ev[4], s));
+    CU(cudaEventRecord(ix->done_ev, s));
+    ix->done_recorded = true;
     ix->events_pending = true;
     ix->last_full_gpu = r.stages == PA_STAGES_FULL_GPU;
     ix->stats = pa_stats{};
@@ -443,8 +453,11 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     if (p->max_degree < 1 || p->max_degree > 64) return fail(PA_EINVAL, "max_degree %d not in 1..64", p->max_degree);
     if (p->metric != PA_L2 && p->metric != PA_IP) return fail(PA_EINVAL, "bad metric %d", p->metric);
     if (p->fes_r < 1 || p->fes_r > 1024) return fail(PA_EINVAL, "fes_r %d not in 1..1024", p->fes_r);
+    if (p->reduced_stride != 0 && p->reduced_stride < p->rdim)
+        return fail(PA_EINVAL, "reduced_stride %lld < rdim %d", (long long)p->reduced_stride, p->rdim);
     const int64_t n = p->n;
     const int D = p->dim, dp = p->rdim;
+    int64_t rsin = p->reduced_stride ? p->reduced_stride : dp;    // input row stride of `reduced`
     // ---- graph and subgraph invariants
     pa_status st = check_csr(p->sub_offsets, p->sub_neighbors, n, p->max_degree, "subgraph");
     if (st != PA_OK) return st;
@@ -478,7 +491,7 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     for (int64_t u = 0; u < n; ++u)
         if (member[u])
             for (int j = 0; j < dp; ++j)
-                if (!std::isfinite(p->reduced[u * dp + j])) return fail(PA_EINVAL, "non-finite reduced[%lld]", (long long)u);
+                if (!std::isfinite(p->reduced[u * rsin + j])) return fail(PA_EINVAL, "non-finite reduced[%lld]", (long long)u);
     // ---- FES index
     const int r = p->fes_r;
     if (p->fes_cell_off[0] != 0) return fail(PA_EFES, "fes_cell_off[0] != 0");
@@ -509,14 +522,16 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
         red16.resize((size_t)n * dp);
         bool bad = false;
         parallel_rows(n, [&](int64_t lo, int64_t hi) {
-            for (int64_t i = lo * dp; i < hi * dp; ++i) {
-                const float v = __half2float(__float2half_rn(p->reduced[i]));
-                red16[i] = v;
-                if (!std::isfinite(v) && member[i / dp]) bad = true;
-            }
+            for (int64_t u = lo; u < hi; ++u)
+                for (int j = 0; j < dp; ++j) {
+                    const float v = __half2float(__float2half_rn(p->reduced[u * rsin + j]));
+                    red16[u * dp + j] = v;
+                    if (!std::isfinite(v) && member[u]) bad = true;
+                }
         });
         if (bad) return fail(PA_EINVAL, "reduced value outside the binary16 range");
         RED = red16.data();
+        rsin = dp;
     }
     // ---- device replica
     int ndev = 0;
@@ -561,6 +576,7 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
     CUB(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
     CUB(cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking));
     for (auto& e : ix->ev) CUB(cudaEventCreate(&e));
+    CUB(cudaEventCreateWithFlags(&ix->done_ev, cudaEventDisableTiming));
     CUB(dalloc(&d.basis, (size_t)D * D));
     CUB(cudaMemcpy(d.basis, p->basis, sizeof(float) * D * D, cudaMemcpyHostToDevice));
     // reduced vectors [n][dps] fp32 or [n][rdim_h] binary16 (zero rows for non-members), staged in chunks
@@ -585,11 +601,11 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
                     if (f16) {
                         __half* dh = &hb[(size_t)i * rs];
                         for (int j = 0; j < rs; ++j)
-                            dh[j] = __float2half_rn(member[u] && j < dp ? RED[u * dp + j] : 0.f);
+                            dh[j] = __float2half_rn(member[u] && j < dp ? RED[u * rsin + j] : 0.f);
                     } else {
                         float* dst = &rb[(size_t)i * rs];
                         if (member[u]) {
-                            std::memcpy(dst, RED + u * dp, sizeof(float) * dp);
+                            std::memcpy(dst, RED + u * rsin, sizeof(float) * dp);
                             for (int j = dp; j < rs; ++j) dst[j] = 0.f;
                         } else {
                             std::memset(dst, 0, sizeof(float) * rs);
@@ -622,13 +638,13 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
         CUB(cudaMemcpy(d.pool_ids, p->fes_pool_ids, sizeof(int32_t) * pool_n, cudaMemcpyHostToDevice));
         std::vector<float> pv((size_t)pool_n * dps, 0.f);
         for (int64_t j = 0; j < pool_n; ++j)
-            std::memcpy(&pv[(size_t)j * dps], RED + (int64_t)p->fes_pool_ids[j] * dp, sizeof(float) * dp);
+            std::memcpy(&pv[(size_t)j * dps], RED + (int64_t)p->fes_pool_ids[j] * rsin, sizeof(float) * dp);
         CUB(dalloc(&d.pool_vec, pv.size()));
         CUB(cudaMemcpy(d.pool_vec, pv.data(), sizeof(float) * pv.size(), cudaMemcpyHostToDevice));
         std::vector<float> pn((size_t)pool_n);
         for (int64_t j = 0; j < pool_n; ++j) {
             double s2 = 0;
-            const float* e = RED + (int64_t)p->fes_pool_ids[j] * dp;
+            const float* e = RED + (int64_t)p->fes_pool_ids[j] * rsin;
             for (int i = 0; i < dp; ++i) s2 += (double)e[i] * e[i];
             pn[j] = (float)s2;
         }
@@ -655,7 +671,7 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
             const int64_t b = p->fes_cell_off[c], nc = p->fes_cell_off[c + 1] - b;
             for (int64_t e = 0; e < nc; ++e) {
                 const int ch = choff[c] + (int)(e / 128), row = (int)(e % 128);
-                const float* src = RED + (int64_t)p->fes_pool_ids[b + e] * dp;
+                const float* src = RED + (int64_t)p->fes_pool_ids[b + e] * rsin;
                 for (int kc = 0; kc < kch; ++kc) {
                     float* hi = &img[(((size_t)ch * kch + kc) * 2 + 0) * 4096];
                     float* lo = &img[(((size_t)ch * kch + kc) * 2 + 1) * 4096];
@@ -889,6 +905,8 @@ pa_status pa_search_candidates(pa_index* ix, const float* queries, int64_t m, in
     pa_status st = resolve(opts, 1, ef, &r, ix->dev.n);
     if (st != PA_OK) return st;
     if (opts && opts->ef1 && opts->ef1 != ef) return fail(PA_EINVAL, "candidates are [m][ef]: ef1 must equal ef");
+    if (r.stages != PA_STAGES_GPU)
+        return fail(PA_EINVAL, "pa_search_candidates returns stage-1 lists: stages must be 0 or PA_STAGES_GPU");
     std::lock_guard<std::mutex> g(ix->mu);
     if (m == 0) return PA_OK;
     return search_host_impl(ix, queries, m, 1, r, cand_ids, cand_dists, true);
@@ -943,6 +961,7 @@ void pa_destroy(pa_index* ix) {
     cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
     cudaFree(d.pool_img); cudaFree(d.chunk_off); cudaFree(d.full_ell); cudaFree(d.xhat);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
+    if (ix->done_ev) cudaEventDestroy(ix->done_ev);
     for (auto e : ix->pipe_done) cudaEventDestroy(e);
     for (auto e : ix->pipe_copied) cudaEventDestroy(e);
     if (ix->pipe_start) cudaEventDestroy(ix->pipe_start);

@@ -70,3 +70,31 @@ def s1():
 @pytest.fixture(scope="session")
 def s2():
     return cached_instance("S2")
+
+
+GOLDEN23 = os.path.join(ROOT, "tests", "golden23")
+
+
+def golden23_names():
+    return sorted(n for n in os.listdir(GOLDEN23) if n.endswith(".json"))
+
+
+def load_golden23(name):
+    with open(os.path.join(GOLDEN23, name)) as f:
+        return json.load(f)
+
+
+def instance_from_golden23(g):
+    """Stages ②③ goldens: separate subgraph / full graph, member flags, d' < D."""
+    x = np.array(g["x"], np.float32)
+    n, D = x.shape
+    dp = g["dp"]
+    soff, snb = csr(g["sub_adjacency"], n)
+    foff, fnb = csr(g["full_adjacency"], n)
+    pool = np.array(g["fes"]["pool"], np.int32)
+    return dict(metric=g["metric"], N=n, D=D, dp=dp, sub_offsets=soff, sub_neighbors=snb,
+                member_flags=np.array(g["members"], np.uint8), reduced=np.ascontiguousarray(x[:, :dp]),
+                rotated=x.copy(), basis=np.array(g["V"], np.float32),
+                fes_centroids=np.array(g["fes"]["centroids"], np.float32),
+                fes_cell_off=np.array([0, pool.size], np.int64), fes_pool_ids=pool,
+                full_offsets=foff, full_neighbors=fnb, queries=np.array([g["query"]], np.float32))

@@ -46,20 +46,20 @@ def compare(inst, gpu: dict, ref: dict, k: int, ef: int, gt_ids=None, check_trac
     Qh = orc.project(inst["queries"], inst["basis"])
     dp = inst["reduced"].shape[1]
     Qp = Qh[:, :dp]
-    X = inst["reduced"].astype(np.float64)
+    Xr = inst["reduced"]                   # may be a strided view (X̂[:, :d'] at 100M): rows gathered on demand
     m = Qp.shape[0]
     rep = ParityReport()
 
     def delta(q, ids):
         ids = np.asarray(ids, dtype=np.int64)
-        x = X[ids]
+        x = Xr[ids].astype(np.float64)
         return ((x - Qp[q]) ** 2).sum(1) if metric == "l2" else -(x @ Qp[q])
 
     def tol(q, ids, d):
         qn2 = float((Qp[q] ** 2).sum())
         if metric == "l2":
             return _tol(d, qn2)
-        sc = np.abs(X[np.asarray(ids, np.int64)] * Qp[q]).sum(1)
+        sc = np.abs(Xr[np.asarray(ids, np.int64)].astype(np.float64) * Qp[q]).sum(1)
         return _tol(d, qn2, sc)
 
     def near(q, a, b):
