@@ -141,7 +141,7 @@ def partition(X: torch.Tensor, ids: torch.Tensor, K: int, seed: int, iters: int 
 # Candidates: exact scoring against the members of the P nearest partitions
 # ----------------------------------------------------------------------------
 def knn_candidates(X: torch.Tensor, ids: torch.Tensor, lab: torch.Tensor, cent: torch.Tensor, L: int,
-                   P: int, batch_elems: float = 6e8) -> torch.Tensor:
+                   P: int, batch_elems: float = 6e8, gather_rows: float = 3e6, a_max: int = 2048) -> torch.Tensor:
     """For every row u of `ids`: the L nearest (squared L2) among the members of
     the P partitions whose centres are nearest to u's partition centre (u's own
     included), self excluded, ascending.  Scores are a TF32 GEMM
@@ -170,34 +170,35 @@ def knn_candidates(X: torch.Tensor, ids: torch.Tensor, lab: torch.Tensor, cent: 
         r = X[ids[s:s + (1 << 22)]]
         xn[s:s + (1 << 22)] = (r * r).sum(1)
     out = torch.full((n, L), -1, dtype=torch.int32, device=dev)
-    # partitions in descending size so a batch pads little
+    # work items = (partition, first row, rows ≤ a_max), partitions in descending size so a batch pads little
     porder = torch.argsort(counts, descending=True).tolist()
     cnt_l = counts.tolist()
-    tot = counts[nbr].sum(1)                                          # candidates per partition
-    tot_l = tot.tolist()
+    tot_l = counts[nbr].sum(1).tolist()                               # candidates per partition
+    items = []
+    for j in porder:
+        if cnt_l[j] == 0:
+            break
+        for a0 in range(0, cnt_l[j], a_max):
+            items.append((j, a0, min(a_max, cnt_l[j] - a0)))
     prof = _Prof()
     prof.tick("start")
     i = 0
-    while i < K:
-        j0 = porder[i]
-        if cnt_l[j0] == 0:
-            break
-        La = cnt_l[j0]
-        b = 1
-        Lc = tot_l[j0]
-        while i + b < K and cnt_l[porder[i + b]] > 0:
-            Lc2 = max(Lc, tot_l[porder[i + b]])
-            if (b + 1) * La * Lc2 > batch_elems:
+    while i < len(items):
+        La, Lc, b = items[i][2], tot_l[items[i][0]], 1
+        while i + b < len(items):
+            La2, Lc2 = max(La, items[i + b][2]), max(Lc, tot_l[items[i + b][0]])
+            if (b + 1) * La2 * Lc2 > batch_elems or (b + 1) * Lc2 > gather_rows:
                 break
-            Lc = Lc2
+            La, Lc = La2, Lc2
             b += 1
-        parts = torch.tensor(porder[i:i + b], device=dev)
+        it = torch.tensor(items[i:i + b], device=dev)                     # [b][3]
         i += b
-        # A rows: members of each partition, padded to La
+        parts, ia0, ila = it[:, 0], it[:, 1:2], it[:, 2:3]
+        # A rows: this item's rows of its partition, padded to La
         pa_ = parts[:, None]
         ta = torch.arange(La, device=dev)[None, :]
-        va = ta < counts[pa_]
-        aidx = torch.where(va, order[(starts[pa_] + ta).clamp_max(n - 1)], torch.zeros_like(ta))
+        va = ta < ila
+        aidx = torch.where(va, order[(starts[pa_] + ia0 + ta).clamp_max(n - 1)], torch.zeros_like(ta))
         # candidate rows: concatenated members of the P nearest partitions, padded to Lc
         nb = nbr[parts]                                                  # [b][P]
         cc = counts[nb]
@@ -372,20 +373,34 @@ def reverse_fill(X: torch.Tensor, ids: torch.Tensor, rows: torch.Tensor, R: int,
 
 
 def build_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor], seed: int, P: int = 0,
-                part_size: int = 1000, slack: int = 32) -> torch.Tensor:
+                part_size: int = 1000, slack: int = 16, labels: Optional[torch.Tensor] = None) -> torch.Tensor:
     """The graph tool at scale (same three steps as `datagen.build_graph`):
-    partition (≈part_size rows per cell) → 2R + slack TF32 candidates from the P
-    nearest partitions → exact re-rank + occlusion pruning to R → reverse fill.
+    partition → 2R + slack TF32 candidates from the members of the P nearest
+    partitions (≈ P·part_size candidates per row) → neighbour-of-neighbour
+    refinement → exact re-rank + occlusion pruning to R → reverse fill.
+    Partitions: k-means cells of ≈part_size rows ("geo", default), or the
+    generation clusters `labels` ("gen", PA_KNN_PART=gen: balanced, no k-means).
     → rows [n][R] int32 global ids aligned with `ids` (all rows if None)."""
     dev = X.device
     if ids is None:
         ids = torch.arange(X.shape[0], device=dev)
     n = ids.numel()
     P = P or int(os.environ.get("PA_KNN_P", "48"))
-    K = max(1, n // part_size)
     t = time.time()
-    lab, cent = partition(X, ids, K, seed)
-    _log(f"graph n={n}: partition K={K} {time.time() - t:.1f}s")
+    if labels is not None and os.environ.get("PA_KNN_PART", "geo") == "gen":
+        lab = labels[ids]
+        K = int(labels.max().item()) + 1
+        cnt = torch.bincount(lab, minlength=K)
+        cent = torch.zeros(K, X.shape[1], dtype=torch.float32, device=dev)
+        for s in range(0, n, 1 << 22):
+            cent.index_add_(0, lab[s:s + (1 << 22)], X[ids[s:s + (1 << 22)]])
+        cent /= cnt.clamp_min(1)[:, None].float()
+        P = min(K, int(math.ceil(P * part_size / max(1.0, n / max(1, int((cnt > 0).sum().item()))))))
+        _log(f"graph n={n}: generation-cluster partitions K={K}, P={P}")
+    else:
+        K = max(1, n // part_size)
+        lab, cent = partition(X, ids, K, seed)
+        _log(f"graph n={n}: partition K={K} {time.time() - t:.1f}s")
     t = time.time()
     cand = knn_candidates(X, ids, lab, cent, 2 * R + slack, P)
     del lab, cent
@@ -479,24 +494,25 @@ def build_instance_large(cfg, device="cuda", cache: Optional[str] = None, gt_k: 
              "fes_centroids", "fes_cell_off", "fes_pool_ids", "gt_ids", "gt_sub_ids")
     hit = cdir and all(os.path.exists(os.path.join(cdir, f + ".npy")) for f in names + ("done",))
     Xh, labels, V, Q = gen_rotated(cfg, device)
-    del labels
     _log(f"{cfg.name}: vectors generated + rotated in {time.time() - t0:.1f}s")
     inst = dict(cfg=cfg, N=cfg.N, D=cfg.D, dp=cfg.dp, metric=cfg.metric, basis=V.astype(np.float32), V64=V,
                 queries=Q.cpu().numpy())
     if hit:
+        del labels
         for f in names:
             inst[f] = np.load(os.path.join(cdir, f + ".npy"))
         _log(f"{cfg.name}: graphs + GT loaded from {cdir} ({time.time() - t0:.1f}s)")
     else:
         t = time.time()
-        full = build_graph(Xh, cfg.R, None, cfg.seeds["graph"])
+        full = build_graph(Xh, cfg.R, None, cfg.seeds["graph"], labels=labels)
         _log(f"{cfg.name}: full graph {time.time() - t:.1f}s")
         flags = sample_members(full, cfg.N, cfg.ratio, cfg.seeds["sample"])
         inst["full_offsets"], inst["full_neighbors"] = rows_to_csr(full, cfg.N)
         del full
         mem = torch.from_numpy(np.flatnonzero(flags)).to(Xh.device)
         t = time.time()
-        sub = build_graph(Xh, cfg.R, mem, cfg.seeds["graph"] + 1)
+        sub = build_graph(Xh, cfg.R, mem, cfg.seeds["graph"] + 1, labels=labels)
+        del labels
         _log(f"{cfg.name}: subgraph ({mem.numel()} members) {time.time() - t:.1f}s")
         inst["sub_offsets"], inst["sub_neighbors"] = rows_to_csr(sub, cfg.N, ids=mem)
         del sub

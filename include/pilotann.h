@@ -186,6 +186,41 @@ pa_status pa_search_device(pa_index* ix, const float* d_queries, int64_t m, int3
 pa_status pa_search_candidates(pa_index* ix, const float* queries, int64_t m, int32_t ef,
                                const pa_search_opts* opts, int32_t* cand_ids, float* cand_dists);
 
+/* ---------------------------------------------------------------------------
+ * Replication across GPUs: queries are independent, so
+ * every GPU holds a full replica of the device index and searches its own shard.
+ * The index is built ONCE (pa_build on the first GPU); the other processes
+ * allocate an empty replica with the same layout and receive the device arrays
+ * over NVLink (e.g. an NCCL broadcast of every buffer pa_replica_buffers lists).
+ * A replica has no host copy of the subgraph, so it serves PA_STAGES_GPU and
+ * PA_STAGES_FULL_GPU (if the source had uploaded the full graph and X̂ before
+ * its meta was exported) but not the host stages (PA_ESTATE).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int64_t n, pool_n;
+    int32_t dim, rdim, rdim_pad, rdim_h, qlen, rstride, rstride_h, ell_w, metric, fes_r;
+    int32_t max_cell, proj_nb, pool_chunks, fes_fold_norm, reduced_fp16;
+    int32_t has_full, full_w, xstride;    /* device copies of the full graph and X̂ (NEXT-f3) */
+} pa_replica_meta;
+
+typedef struct {
+    void* ptr;       /* DEVICE pointer on the index's device */
+    int64_t bytes;
+} pa_buffer;
+
+/* Layout of a built index (PA_ESTATE on a bad handle). */
+pa_status pa_replica_meta_of(const pa_index* ix, pa_replica_meta* out);
+
+/* Allocate an EMPTY replica with the layout `meta` on `device` (contents
+ * undefined until every buffer of pa_replica_buffers has been filled with the
+ * source's bytes).  PA_EINVAL for an inconsistent meta, PA_ENOMEM if it does not fit. */
+pa_status pa_build_replica(const pa_replica_meta* meta, int32_t device, pa_index** out);
+
+/* The index's read-only device arrays, in a fixed order that is identical for
+ * a source and a replica of the same meta: writes min(cap, total) entries of
+ * out[] and the total count to *count. */
+pa_status pa_replica_buffers(pa_index* ix, pa_buffer* out, int32_t cap, int32_t* count);
+
 /* Copy the last search's pa_stats into *out (size = sizeof(pa_stats)). */
 pa_status pa_get_stats(const pa_index* ix, pa_stats* out, size_t size);
 

@@ -31,7 +31,8 @@ PA_NO_FES, PA_NO_STAGE2, PA_NO_STAGE1, PA_NO_PIPELINE = 1, 2, 4, 8
 
 # Symbols declared in include/pilotann.h (checked by tests/test_abi.py).
 EXPORTS = ("pa_build", "pa_attach_host", "pa_search", "pa_search_device", "pa_search_candidates",
-           "pa_get_stats", "pa_destroy", "pa_last_error", "pa_version")
+           "pa_get_stats", "pa_destroy", "pa_last_error", "pa_version",
+           "pa_replica_meta_of", "pa_build_replica", "pa_replica_buffers")
 
 
 class PAError(RuntimeError):
@@ -54,6 +55,23 @@ class SearchOpts(C.Structure):
                 ("entries", C.c_int32), ("width", C.c_int32), ("refine_iters", C.c_int32),
                 ("flags", C.c_uint32), ("hash_slots_log2", C.c_int32), ("host_threads", C.c_int32),
                 ("bloom_log2", C.c_int32)]
+
+
+class ReplicaMeta(C.Structure):
+    _fields_ = [("n", C.c_int64), ("pool_n", C.c_int64)] + [(f, C.c_int32) for f in (
+        "dim", "rdim", "rdim_pad", "rdim_h", "qlen", "rstride", "rstride_h", "ell_w", "metric", "fes_r",
+        "max_cell", "proj_nb", "pool_chunks", "fes_fold_norm", "reduced_fp16", "has_full", "full_w", "xstride")]
+
+    def to_list(self):
+        return [getattr(self, f) for f, _ in self._fields_]
+
+    @classmethod
+    def from_list(cls, vals):
+        return cls(**{f: int(v) for (f, _), v in zip(cls._fields_, vals)})
+
+
+class Buffer(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("bytes", C.c_int64)]
 
 
 class Debug(C.Structure):
@@ -102,6 +120,12 @@ def lib():
         L.pa_get_stats.argtypes = [vp, C.POINTER(Stats), C.c_size_t]
         L.pa_destroy.restype = None
         L.pa_destroy.argtypes = [vp]
+        L.pa_replica_meta_of.restype = C.c_int
+        L.pa_replica_meta_of.argtypes = [vp, C.POINTER(ReplicaMeta)]
+        L.pa_build_replica.restype = C.c_int
+        L.pa_build_replica.argtypes = [C.POINTER(ReplicaMeta), i32, C.POINTER(vp)]
+        L.pa_replica_buffers.restype = C.c_int
+        L.pa_replica_buffers.argtypes = [vp, C.POINTER(Buffer), i32, C.POINTER(i32)]
         L.pa_last_error.restype = C.c_char_p
         L.pa_version.restype = C.c_char_p
         _lib = L
@@ -206,6 +230,32 @@ class Index:
                    fes_cell_off=inst["fes_cell_off"], fes_pool_ids=inst["fes_pool_ids"],
                    member_flags=inst.get("member_flags"), metric=inst.get("metric", "l2"),
                    max_degree=max_degree, device=device, reduced_fp16=reduced_fp16)
+
+    # -- replication (pa_replica_meta_of / pa_build_replica / pa_replica_buffers) --
+    def replica_meta(self) -> ReplicaMeta:
+        m = ReplicaMeta()
+        _check(lib().pa_replica_meta_of(self._h, C.byref(m)))
+        return m
+
+    @classmethod
+    def empty_replica(cls, meta: ReplicaMeta, device: int) -> "Index":
+        """An unfilled replica with `meta`'s layout on `device` (fill every buffer, e.g. by broadcast)."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        _check(lib().pa_build_replica(C.byref(meta), int(device), C.byref(h)))
+        self._h = h
+        self.n, self.dim, self.rdim, self.device = int(meta.n), int(meta.dim), int(meta.rdim), int(device)
+        self.metric = "ip" if meta.metric == PA_IP else "l2"
+        self._host_keep = None
+        return self
+
+    def replica_buffers(self) -> list[tuple[int, int]]:
+        """[(device pointer, bytes)] of the replica's device arrays, in the fixed ABI order."""
+        cnt = C.c_int32()
+        _check(lib().pa_replica_buffers(self._h, None, 0, C.byref(cnt)))
+        arr = (Buffer * cnt.value)()
+        _check(lib().pa_replica_buffers(self._h, arr, cnt.value, C.byref(cnt)))
+        return [(int(b.ptr or 0), int(b.bytes)) for b in arr]
 
     # -- pa_attach_host -----------------------------------------------------
     def attach_host(self, full_offsets, full_neighbors, rotated):

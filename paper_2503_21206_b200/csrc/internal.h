@@ -25,13 +25,16 @@ struct DevIndex {
     int32_t* cell_off = nullptr;               // [r+1]
     int32_t* pool_ids = nullptr;               // [pool_n] grouped by cell
     float* pool_vec = nullptr;                 // [pool_n][rdim_pad] contiguous by cell
-    float* proj_bt = nullptr;                  // [roundup16(r + dim)][dim] B_T of the tcgen05 projection
+    float* proj_img = nullptr;                 // [ceil(dim/32)][hi,lo][proj_nb][32] B_T of the tcgen05 projection,
+                                               // split to TF32 hi/lo, rows K-major SWIZZLE_128B (TMA bulk sources)
+    int32_t proj_nb = 0;                       // rows of B_T: roundup16(r + dim)
     float* cent_norm = nullptr;                // [r] ‖centroid‖²
     float* pool_norm = nullptr;                // [pool_n] ‖e‖² (GEMM-form FES scores)
     int32_t max_cell = 0;                      // largest FES cell (score scratch row stride, multiple of 4)
     float* pool_img = nullptr;                 // [chunks][kch][hi,lo][4096]: pool split to TF32 hi/lo and laid
                                                // out as K-major SWIZZLE_128B 128×32 tiles (TMA bulk sources)
     int32_t* chunk_off = nullptr;              // [r+1] first 128-entry pool chunk of each cell
+    int32_t pool_chunks = 0;                   // total 128-entry pool chunks (= chunk_off[r])
     // NEXT-f3 (PA_STAGES_FULL_GPU), uploaded on first use from pa_attach_host's arrays
     int32_t* full_ell = nullptr;               // [n][full_w] full graph, −1 padded
     int32_t full_w = 0;

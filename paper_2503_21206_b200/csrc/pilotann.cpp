@@ -432,6 +432,29 @@ pa_status ensure_host_ws(pa_index* ix, int64_t m, int32_t ef) {
     return PA_OK;
 }
 
+// The replica's device arrays in a fixed order (pa_replica_buffers): pointer slot + bytes.
+void replica_list(pa::DevIndex& d, std::vector<std::pair<void**, size_t>>& L) {
+    const size_t n = (size_t)d.n, r = (size_t)d.fes_r, dps = (size_t)d.rdim_pad, D = (size_t)d.dim;
+    auto add = [&](auto** p, size_t bytes) { L.emplace_back(reinterpret_cast<void**>(p), bytes); };
+    add(&d.basis, D * D * 4);
+    if (d.reduced_h) add(&d.reduced_h, n * d.rstride_h * 2);
+    else add(&d.reduced, n * d.rstride * 4);
+    add(&d.ell, n * d.ell_w * 4);
+    add(&d.centroids, r * dps * 4);
+    add(&d.cell_off, (r + 1) * 4);
+    add(&d.pool_ids, (size_t)d.pool_n * 4);
+    add(&d.pool_vec, (size_t)d.pool_n * dps * 4);
+    add(&d.pool_norm, (size_t)d.pool_n * 4);
+    add(&d.pool_img, (size_t)d.pool_chunks * ((dps + 31) / 32) * 2 * 4096 * 4);
+    add(&d.chunk_off, (r + 1) * 4);
+    add(&d.proj_img, ((D + 31) / 32) * 2 * (size_t)d.proj_nb * 32 * 4);
+    add(&d.cent_norm, r * 4);
+    if (d.xhat) {
+        add(&d.full_ell, n * d.full_w * 4);
+        add(&d.xhat, n * d.xstride * 4);
+    }
+}
+
 }  // namespace
 
 // ============================================================================ ABI
@@ -692,13 +715,17 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
         }
         CUB(dalloc(&d.pool_img, img.size()));
         CUB(cudaMemcpy(d.pool_img, img.data(), sizeof(float) * img.size(), cudaMemcpyHostToDevice));
+        d.pool_chunks = choff[r];
         CUB(dalloc(&d.chunk_off, choff.size()));
         CUB(cudaMemcpy(d.chunk_off, choff.data(), sizeof(int32_t) * choff.size(), cudaMemcpyHostToDevice));
     }
-    // tcgen05 projection operand B_T = [(V_{:d'}·Cᵀ)ᵀ ; Vᵀ] (rows K-major), fp64 → fp32, zero-padded
+    // tcgen05 projection operand B_T = [(V_{:d'}·Cᵀ)ᵀ ; Vᵀ] (rows K-major), fp64 → fp32, split to TF32
+    // hi/lo and laid out per 32-float K chunk as two planes of [NB][32] in K-major SWIZZLE_128B order
+    // (the same element placement as the FES pool tiles), zero-padded to NB = roundup16(r + D) rows.
     {
-        const int rows = ((r + D) + 15) & ~15;
-        std::vector<float> bt((size_t)rows * D, 0.f);
+        const int NB = ((r + D) + 15) & ~15;
+        const int kch = (D + 31) / 32;
+        std::vector<float> bt((size_t)NB * D, 0.f);
         for (int c = 0; c < r; ++c)
             for (int k = 0; k < D; ++k) {
                 double s = 0;
@@ -707,14 +734,29 @@ pa_status pa_build(const pa_build_params* p, pa_index** out) {
             }
         for (int j = 0; j < D; ++j)
             for (int k = 0; k < D; ++k) bt[(size_t)(r + j) * D + k] = p->basis[(size_t)k * D + j];
+        std::vector<float> img((size_t)kch * 2 * NB * 32, 0.f);
+        for (int n = 0; n < NB; ++n)
+            for (int k = 0; k < kch * 32; ++k) {
+                const float a = k < D ? bt[(size_t)n * D + k] : 0.f;
+                uint32_t bits;
+                std::memcpy(&bits, &a, 4);
+                bits &= 0xFFFFE000u;
+                float h;
+                std::memcpy(&h, &bits, 4);
+                const int kc = k >> 5, kk = k & 31;
+                const size_t in_row = (size_t)n * 32 + ((((kk >> 2) ^ (n & 7)) << 2) | (kk & 3));
+                img[((size_t)kc * 2 + 0) * NB * 32 + in_row] = h;
+                img[((size_t)kc * 2 + 1) * NB * 32 + in_row] = a - h;
+            }
         std::vector<float> cn(r);
         for (int c = 0; c < r; ++c) {
             double s = 0;
             for (int j = 0; j < dp; ++j) s += (double)p->fes_centroids[(size_t)c * dp + j] * p->fes_centroids[(size_t)c * dp + j];
             cn[c] = (float)s;
         }
-        CUB(dalloc(&d.proj_bt, bt.size()));
-        CUB(cudaMemcpy(d.proj_bt, bt.data(), sizeof(float) * bt.size(), cudaMemcpyHostToDevice));
+        d.proj_nb = NB;
+        CUB(dalloc(&d.proj_img, img.size()));
+        CUB(cudaMemcpy(d.proj_img, img.data(), sizeof(float) * img.size(), cudaMemcpyHostToDevice));
         CUB(dalloc(&d.cent_norm, cn.size()));
         CUB(cudaMemcpy(d.cent_norm, cn.data(), sizeof(float) * cn.size(), cudaMemcpyHostToDevice));
     }
@@ -770,6 +812,8 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
     const bool full = !candidates_only && r.stages == PA_STAGES_FULL;
     if (full && (!ix->h_rotated || !ix->h_full_off))
         return fail(PA_ESTATE, "PA_STAGES_FULL requires pa_attach_host");
+    if (full && ix->h_sub_off.empty())
+        return fail(PA_ESTATE, "PA_STAGES_FULL: this replica has no host copy of the subgraph (built by pa_build_replica)");
     if (!candidates_only && r.stages == PA_STAGES_FULL_GPU) {
         pa_status st0 = ensure_full_device(ix);
         if (st0 != PA_OK) return st0;
@@ -912,6 +956,87 @@ pa_status pa_search_candidates(pa_index* ix, const float* queries, int64_t m, in
     return search_host_impl(ix, queries, m, 1, r, cand_ids, cand_dists, true);
 }
 
+pa_status pa_replica_meta_of(const pa_index* ix, pa_replica_meta* out) {
+    g_err.clear();
+    if (!live(ix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
+    if (!out) return fail(PA_EINVAL, "null argument");
+    const auto& d = ix->dev;
+    pa_replica_meta m{};
+    m.n = d.n; m.pool_n = d.pool_n; m.dim = d.dim; m.rdim = d.rdim; m.rdim_pad = d.rdim_pad; m.rdim_h = d.rdim_h;
+    m.qlen = d.qlen; m.rstride = d.rstride; m.rstride_h = d.rstride_h; m.ell_w = d.ell_w; m.metric = d.metric;
+    m.fes_r = d.fes_r; m.max_cell = d.max_cell; m.proj_nb = d.proj_nb; m.pool_chunks = d.pool_chunks;
+    m.fes_fold_norm = d.fes_fold_norm ? 1 : 0; m.reduced_fp16 = d.reduced_h ? 1 : 0;
+    m.has_full = d.xhat ? 1 : 0; m.full_w = d.full_w; m.xstride = d.xstride;
+    *out = m;
+    return PA_OK;
+}
+
+pa_status pa_build_replica(const pa_replica_meta* m, int32_t device, pa_index** out) {
+    g_err.clear();
+    if (!m || !out) return fail(PA_EINVAL, "null argument");
+    *out = nullptr;
+    const bool ok = m->n > 0 && m->n < (1ll << 31) && m->dim > 0 && m->dim <= 4096 && m->rdim > 0 &&
+                    m->rdim <= m->dim && m->rdim_pad == ((m->rdim + 3) & ~3) && m->rstride == ((m->rdim_pad + 31) & ~31) &&
+                    (m->ell_w == 32 || m->ell_w == 64) && (m->metric == PA_L2 || m->metric == PA_IP) &&
+                    m->fes_r >= 1 && m->fes_r <= 1024 && m->pool_n >= m->fes_r && m->pool_chunks >= m->fes_r &&
+                    m->proj_nb == ((m->fes_r + m->dim + 15) & ~15) && m->max_cell > 0 &&
+                    (!m->has_full || ((m->full_w == 32 || m->full_w == 64) && m->xstride == ((m->dim + 31) & ~31)));
+    if (!ok) return fail(PA_EINVAL, "inconsistent replica meta");
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(PA_EINVAL, "device %d not in [0,%d)", device, ndev);
+    CU(cudaSetDevice(device));
+    pa_index* ix = new pa_index();
+    ix->device = device;
+    auto& d = ix->dev;
+    d.n = m->n; d.pool_n = m->pool_n; d.dim = m->dim; d.rdim = m->rdim; d.rdim_pad = m->rdim_pad; d.rdim_h = m->rdim_h;
+    d.qlen = m->qlen; d.rstride = m->rstride; d.rstride_h = m->rstride_h; d.ell_w = m->ell_w; d.metric = m->metric;
+    d.fes_r = m->fes_r; d.max_cell = m->max_cell; d.proj_nb = m->proj_nb; d.pool_chunks = m->pool_chunks;
+    d.fes_fold_norm = m->fes_fold_norm != 0; d.full_w = m->has_full ? m->full_w : 0; d.xstride = m->has_full ? m->xstride : 0;
+    {
+        std::lock_guard<std::mutex> g(g_reg_mu);
+        g_live.insert(ix);
+    }
+    auto bail = [&](pa_status s) { pa_destroy(ix); return s; };
+    // sentinel non-null pointers select the optional arrays in replica_list, then real allocations
+    if (m->reduced_fp16) d.reduced_h = reinterpret_cast<void*>(1);
+    if (m->has_full) d.xhat = reinterpret_cast<float*>(1);
+    std::vector<std::pair<void**, size_t>> L;
+    replica_list(d, L);
+    for (auto& e : L) *e.first = nullptr;
+    for (auto& e : L) {
+        cudaError_t er = cudaMalloc(e.first, std::max<size_t>(1, e.second));
+        if (er != cudaSuccess) {
+            *e.first = nullptr;
+            return bail(fail(er == cudaErrorMemoryAllocation ? PA_ENOMEM : PA_ECUDA, "replica allocation: %s",
+                             cudaGetErrorString(er)));
+        }
+    }
+    if (cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ix->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ix->done_ev, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(PA_ECUDA, "replica streams"));
+    for (auto& e : ix->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(PA_ECUDA, "replica events"));
+    *out = ix;
+    return PA_OK;
+}
+
+pa_status pa_replica_buffers(pa_index* ix, pa_buffer* out, int32_t cap, int32_t* count) {
+    g_err.clear();
+    if (!live(ix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
+    if (!count || (cap > 0 && !out)) return fail(PA_EINVAL, "null argument");
+    std::lock_guard<std::mutex> g(ix->mu);
+    std::vector<std::pair<void**, size_t>> L;
+    replica_list(ix->dev, L);
+    for (int32_t i = 0; i < cap && i < (int32_t)L.size(); ++i) {
+        out[i].ptr = *L[i].first;
+        out[i].bytes = (int64_t)L[i].second;
+    }
+    *count = (int32_t)L.size();
+    return PA_OK;
+}
+
 pa_status pa_get_stats(const pa_index* cix, pa_stats* out, size_t size) {
     g_err.clear();
     if (!live(cix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
@@ -958,7 +1083,7 @@ void pa_destroy(pa_index* ix) {
     cudaFreeHost(ix->h_counters);
     auto& d = ix->dev;
     cudaFree(d.basis); cudaFree(d.reduced); cudaFree(d.reduced_h); cudaFree(d.ell); cudaFree(d.centroids); cudaFree(d.cell_off);
-    cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_bt); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
+    cudaFree(d.pool_ids); cudaFree(d.pool_vec); cudaFree(d.proj_img); cudaFree(d.cent_norm); cudaFree(d.pool_norm);
     cudaFree(d.pool_img); cudaFree(d.chunk_off); cudaFree(d.full_ell); cudaFree(d.xhat);
     for (auto& e : ix->ev) if (e) cudaEventDestroy(e);
     if (ix->done_ev) cudaEventDestroy(ix->done_ev);

@@ -118,7 +118,7 @@ def test_binding_structs_match_the_header(tmp_path):
     offsets (a C program compiled against include/pilotann.h prints them)."""
     import subprocess
     structs = {"pa_build_params": pa.BuildParams, "pa_search_opts": pa.SearchOpts, "pa_debug": pa.Debug,
-               "pa_stats": pa.Stats}
+               "pa_stats": pa.Stats, "pa_replica_meta": pa.ReplicaMeta, "pa_buffer": pa.Buffer}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "pilotann.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
@@ -139,3 +139,14 @@ def test_binding_structs_match_the_header(tmp_path):
         assert C.sizeof(py) == want[(cname, "size")], cname
         for f, _ in py._fields_:
             assert getattr(py, f).offset == want[(cname, f)], (cname, f)
+
+
+def test_replica_meta_rejected_before_device(L):
+    """pa_build_replica validates the layout before touching a device."""
+    m = pa.ReplicaMeta(n=100, pool_n=8, dim=16, rdim=8, rdim_pad=8, rdim_h=8, qlen=8, rstride=32, rstride_h=64,
+                       ell_w=48, metric=0, fes_r=4, max_cell=4, proj_nb=32, pool_chunks=4)
+    h = C.c_void_p()
+    assert L.pa_build_replica(C.byref(m), 0, C.byref(h)) == pa.PA_EINVAL          # ell_w must be 32 or 64
+    assert "inconsistent" in L.pa_last_error().decode()
+    cnt = C.c_int32()
+    assert L.pa_replica_buffers(None, None, 0, C.byref(cnt)) == pa.PA_ESTATE

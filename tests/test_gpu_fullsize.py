@@ -62,3 +62,36 @@ def test_c1_full_size_sampled_parity(c1, ef, bloom):
     want = ((X - Qh[:, None, :]) ** 2).sum(2)
     tol = 1e-5 * want + 1e-6 * np.sqrt(want * (Qh ** 2).sum(1, keepdims=True))
     assert np.all(np.abs(d - want) <= tol)
+
+
+@pytest.fixture(scope="module")
+def ip1m():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__ as g
+    g.build_library()
+    import datagen as dg
+    from datagen import large as lg
+    cfg = dg.get_config("C2S", N=1_000_000, m=1000)
+    return lg.build_instance_large(cfg, device="cuda", gt_k=10)
+
+
+@pytest.mark.parametrize("bloom", [0, 12])
+def test_ip_1m_sampled_parity(ip1m, bloom):
+    """Inner product (T2I shape, OOD queries) at 1M rows through the 100M-scale
+    instance path (strided X̂ rows): sampled tie-aware parity with the oracle and
+    Recall@10 (GT_sub) within 0.002 of the oracle's on the sample."""
+    inst = ip1m
+    cfg = inst["cfg"]
+    ix = pa.Index.from_instance(inst)
+    g = run_gpu(ix, inst, cfg.k, 64, trace_cap=8192, bloom_log2=bloom)
+    ix.close()
+    sample = np.arange(0, inst["queries"].shape[0], 5)
+    sub = dict(inst, queries=inst["queries"][sample])
+    gs = {k: v[sample] for k, v in g.items()}
+    r = orc.search(sub, k=cfg.k, ef=64, stages=1, trace_cap=8192, bloom_log2=bloom or None)
+    rep = compare(sub, gs, r, cfg.k, 64, gt_ids=inst["gt_sub_ids"][sample, :cfg.k])
+    print("IP 1M", bloom, rep, rep.recall_gpu, rep.recall_orc)
+    assert not rep.fail, rep.fail[:5]
+    assert rep.exact >= 0.8 * sample.size

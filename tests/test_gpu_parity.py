@@ -554,3 +554,71 @@ def test_searches_on_two_streams_serialise(s1):
         for (oi, od), (ri, rd) in zip(outs, ref):
             assert torch.equal(oi.cpu(), ri) and torch.equal(od.cpu(), rd)
     ix.close()
+
+
+# ------------------------------------------------- configurations untested in r1 --
+def _full_checks(inst, ids, d, k, r_ids):
+    Qh = orc.project(inst["queries"], inst["basis"])
+    gt, _ = orc.brute_force(Qh, inst["rotated"], k, metric=inst["metric"])
+    rg, ro = orc.recall(ids, gt, k), orc.recall(r_ids, gt, k)
+    assert abs(rg - ro) <= 0.002 + 1e-12, (rg, ro)
+    X = inst["rotated"].astype(np.float64)[ids]
+    want = ((X - Qh[:, None, :]) ** 2).sum(2) if inst["metric"] == "l2" else -(X * Qh[:, None, :]).sum(2)
+    scale = np.abs(want) if inst["metric"] == "l2" else np.abs(X * Qh[:, None, :]).sum(2)
+    assert np.all(np.abs(d - want) <= 1e-5 * scale + 1e-6 * np.sqrt(np.abs(want) * (Qh ** 2).sum(1, keepdims=True)))
+    return rg, ro
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_d768_parity(metric):
+    """LAION/WIKI shape D = 768, d' = 128 (C3/C4): the tcgen05 projection with
+    q_res (r + D = 800 columns, four column tiles) and tcgen05 FES, stage ① tie-aware
+    against the oracle, stages ②③ (host and GPU) by recall and fp64 distances."""
+    inst = tiny_instance(n=2500, D=768, dp=128, R=16, m=130, seed=768, member_ratio=0.5, r=8, metric=metric)
+    for bloom in (0, 12):
+        g, r = _both(inst, 10, 48, trace_cap=8192, bloom_log2=bloom)
+        rep = compare(inst, g, r, 10, 48)
+        assert not rep.fail, rep.fail[:3]
+        assert rep.exact >= 0.9 * 130
+    ix = pa.Index.from_instance(inst)
+    ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
+    r3 = orc.search(inst, k=10, ef=48, stages=3)
+    for stages in (pa.PA_STAGES_FULL, pa.PA_STAGES_FULL_GPU):
+        ids, d = ix.search(inst["queries"], k=10, ef=48, stages=stages)
+        print(metric, stages, _full_checks(inst, ids, d, 10, r3["ids"]))
+    ix.close()
+
+
+@pytest.mark.parametrize("bloom", [0, 12])
+def test_ids_above_2pow24(bloom):
+    """Member ids ≥ 2^24 (100M-scale id space): the exact kernels switch to the
+    wide (32-bit) visited hash; parity with the oracle, tie-aware, plus stage ②③
+    on the GPU."""
+    from tiny import sparse_id_instance
+    inst = sparse_id_instance()
+    assert inst["fes_pool_ids"].max() >= (1 << 24)
+    g, r = _both(inst, 10, 64, trace_cap=8192, bloom_log2=bloom)
+    rep = compare(inst, g, r, 10, 64)
+    assert not rep.fail, rep.fail[:3]
+    assert rep.exact >= 0.9 * inst["queries"].shape[0]
+    assert (g["ids"] >= (1 << 24)).any()
+
+
+def test_degree_64_parity():
+    """Subgraph degrees up to 64 (ELL width 64, the ABI's max_degree bound): exact
+    visited set, tie-aware parity; the bloom filter rejects width 64 (PA_ENOTSUP)."""
+    inst = tiny_instance(n=3000, D=32, dp=16, R=64, m=96, seed=64, member_ratio=0.6, r=8)
+    assert np.diff(inst["sub_offsets"]).max() > 32
+    g, r = _both(inst, 10, 64, trace_cap=16384)
+    rep = compare(inst, g, r, 10, 64)
+    assert not rep.fail, rep.fail[:3]
+    assert rep.exact >= 0.9 * 96
+    ix = pa.Index.from_instance(inst)
+    with pytest.raises(pa.PAError) as e:
+        run_gpu(ix, inst, 10, 64, bloom_log2=12)
+    assert e.value.status == pa.PA_ENOTSUP
+    ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
+    ids, d = ix.search(inst["queries"], k=10, ef=64, stages=pa.PA_STAGES_FULL_GPU)
+    r3 = orc.search(inst, k=10, ef=64, stages=3)
+    _full_checks(inst, ids, d, 10, r3["ids"])
+    ix.close()

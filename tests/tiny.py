@@ -52,3 +52,33 @@ def tiny_instance(n=200, D=16, dp=8, R=8, m=16, seed=1, metric="l2", r=4, member
                 basis=V.astype(np.float32), fes_centroids=cent, fes_cell_off=cuts,
                 fes_pool_ids=pool.astype(np.int32), full_offsets=full_off,
                 full_neighbors=full_nb.astype(np.int32), queries=Q)
+
+
+def sparse_id_instance(n_total=(1 << 24) + 4096, members=3000, D=16, dp=8, R=16, m=48, seed=11, metric="l2",
+                       r=4):
+    """Members scattered over a full id space larger than 2^24 (about a third of
+    them ≥ 2^24): exercises the wide-id visited hash of the exact kernels.
+    Non-member rows are zero; `reduced` is the strided view X̂[:, :d']."""
+    rng = np.random.Generator(np.random.Philox(key=seed))
+    lo = rng.choice(1 << 24, size=members - members // 3, replace=False)
+    hi = (1 << 24) + rng.choice(n_total - (1 << 24), size=members // 3, replace=False)
+    mem = np.sort(np.concatenate([lo, hi])).astype(np.int64)
+    V = orthonormal(D, seed)
+    Xm = rng.standard_normal((mem.size, D))
+    Xh = np.zeros((n_total, D), np.float32)
+    Xh[mem] = (Xm @ V).astype(np.float32)
+    _, o2, nb2 = dg.ring_graph_fixture(mem.size, R, 1, seed + 5)
+    deg = np.zeros(n_total, np.int64)
+    deg[mem] = np.diff(o2)
+    off = np.zeros(n_total + 1, np.int64)
+    np.cumsum(deg, out=off[1:])
+    nb = mem[nb2].astype(np.int32)                       # rows in ascending member order = ascending id order
+    flags = np.zeros(n_total, np.uint8)
+    flags[mem] = 1
+    cuts = np.linspace(0, mem.size, r + 1).astype(np.int64)
+    Xr = Xh[:, :dp]
+    cent = np.stack([Xr[mem[cuts[c]:cuts[c + 1]]].astype(np.float64).mean(0) for c in range(r)]).astype(np.float32)
+    Q = rng.standard_normal((m, D)).astype(np.float32)
+    return dict(metric=metric, N=n_total, D=D, dp=dp, sub_offsets=off, sub_neighbors=nb, member_flags=flags,
+                reduced=Xr, rotated=Xh, basis=V.astype(np.float32), fes_centroids=cent, fes_cell_off=cuts,
+                fes_pool_ids=mem.astype(np.int32), queries=Q)
