@@ -410,7 +410,7 @@ def build_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor], seed: int,
         cand = refine(X, ids, cand, fan=int(os.environ.get("PA_KNN_FAN", "8")))
         _log(f"graph n={n}: refine pass {time.time() - t:.1f}s")
     t = time.time()
-    rows = prune(X, ids, cand, R, 2 * R)
+    rows = prune(X, ids, cand, R, 2 * R, alpha=float(os.environ.get("PA_GRAPH_ALPHA", "1.0")))
     del cand
     _log(f"graph n={n}: prune {time.time() - t:.1f}s")
     t = time.time()
@@ -517,7 +517,7 @@ def build_instance_large(cfg, device="cuda", cache: Optional[str] = None, gt_k: 
         inst["sub_offsets"], inst["sub_neighbors"] = rows_to_csr(sub, cfg.N, ids=mem)
         del sub
         inst["member_flags"] = flags
-        Xr = Xh[:, :cfg.dp]
+        Xr = Xh[:, :cfg.dp]                                # view: deleted before X̂ is released
         inst["fes_centroids"], inst["fes_cell_off"], inst["fes_pool_ids"] = dg.train_fes(
             Xr, flags, cfg.r, cfg.n_e, cfg.seeds["fes"], metric=cfg.metric)
         if with_gt:
@@ -526,7 +526,7 @@ def build_instance_large(cfg, device="cuda", cache: Optional[str] = None, gt_k: 
             inst["gt_ids"], _ = dg.ground_truth(Qh, Xh, gt_k, cfg.metric)
             inst["gt_sub_ids"], _ = dg.ground_truth(Qh[:, :cfg.dp], Xr, gt_k, cfg.metric, ids=mem)
             _log(f"{cfg.name}: ground truth {time.time() - t:.1f}s")
-        del mem
+        del mem, Xr
         if cdir:
             os.makedirs(cdir, exist_ok=True)
             for f in names:

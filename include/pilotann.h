@@ -121,7 +121,13 @@ typedef struct {
                                 0x85EBCA77, 0xC2B2AE3D).  False positives skip nodes (stages ②③ keep exact
                                 sets and re-visit); results then match the oracle's O13 mode.
                                 Requires max_degree ≤ 32 (PA_ENOTSUP otherwise); other values PA_EINVAL. */
+    uint32_t check_path;     /* test hooks that select a cross-check implementation (results must not change):
+                                PA_CHECK_SIMT = run the SIMT fp32 projection + FES kernels instead of the tcgen05
+                                ones; PA_CHECK_WIDE_VISITED = 32-bit exact visited table even when ids < 2^24.
+                                0 for normal use. */
 } pa_search_opts;
+
+enum { PA_CHECK_SIMT = 1u, PA_CHECK_WIDE_VISITED = 2u };
 
 /* Optional per-query debug/trace outputs of stage ① (DEVICE pointers, may be
  * NULL individually).  Trace mode is for parity tests, never for timed runs. */

@@ -28,6 +28,7 @@ STATUS_NAMES = {0: "PA_OK", -1: "PA_EINVAL", -2: "PA_EGRAPH", -3: "PA_EBASIS", -
 PA_L2, PA_IP = 0, 1
 PA_STAGES_GPU, PA_STAGES_FULL, PA_STAGES_FULL_GPU = 1, 3, 7
 PA_NO_FES, PA_NO_STAGE2, PA_NO_STAGE1, PA_NO_PIPELINE = 1, 2, 4, 8
+PA_CHECK_SIMT, PA_CHECK_WIDE_VISITED = 1, 2
 
 # Symbols declared in include/pilotann.h (checked by tests/test_abi.py).
 EXPORTS = ("pa_build", "pa_attach_host", "pa_search", "pa_search_device", "pa_search_candidates",
@@ -54,7 +55,7 @@ class SearchOpts(C.Structure):
     _fields_ = [("stages", C.c_int32), ("ef1", C.c_int32), ("ef2", C.c_int32), ("ef3", C.c_int32),
                 ("entries", C.c_int32), ("width", C.c_int32), ("refine_iters", C.c_int32),
                 ("flags", C.c_uint32), ("hash_slots_log2", C.c_int32), ("host_threads", C.c_int32),
-                ("bloom_log2", C.c_int32)]
+                ("bloom_log2", C.c_int32), ("check_path", C.c_uint32)]
 
 
 class ReplicaMeta(C.Structure):
@@ -186,10 +187,10 @@ def _dev_rows(x, rows, cols, dtype, device, name):
 
 
 def make_opts(stages=PA_STAGES_GPU, ef1=0, ef2=0, ef3=0, entries=0, width=0, refine_iters=0, flags=0,
-              hash_slots_log2=0, host_threads=0, bloom_log2=0) -> SearchOpts:
+              hash_slots_log2=0, host_threads=0, bloom_log2=0, check_path=0) -> SearchOpts:
     return SearchOpts(stages=stages, ef1=ef1, ef2=ef2, ef3=ef3, entries=entries, width=width,
                       refine_iters=refine_iters, flags=flags, hash_slots_log2=hash_slots_log2,
-                      host_threads=host_threads, bloom_log2=bloom_log2)
+                      host_threads=host_threads, bloom_log2=bloom_log2, check_path=check_path)
 
 
 class Index:

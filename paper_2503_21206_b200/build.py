@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
         return LIB
     os.makedirs(OBJ, exist_ok=True)
-    extra = [f"-D{k}={os.environ[k]}" for k in ("PA_TRAV_MINB", "PA_TRAV_MINB_BLOOM", "PA_ROW_GROUP", "PA_GROUP_L32", "PA_GROUP_L16", "PA_SEL_MINB", "PA_SEL_NV", "PA_MERGE_FIRST", "PA_SPEC", "PA_ROWPF", "PA_REFINE_L", "PA_REFINE_MINB", "PA_ELLPF") if os.environ.get(k)]
+    extra = []          # the kernels' tuning constants are fixed in the sources
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         outs = list(ex.map(lambda s: _compile(s, extra), _sources()))
     objs = [o for o, _ in outs]

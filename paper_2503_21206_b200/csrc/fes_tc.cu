@@ -4,11 +4,11 @@
 // routed elsewhere ("allocation-free").  Here:
 //   k_bucket  : stable counting sort of the queries by routed cell → perm,
 //               per-cell query offsets and per-cell 128-query tile offsets (a3).
-//   k_fes_scores : one CTA per (cell, 128 routed queries) tile — a grouped GEMM
+//   k_fes_scores_tma : one CTA per (cell, 128 routed queries) tile — a grouped GEMM
 //               S = Q'_tile · EV_cellᵀ on tcgen05 (kind::tf32, 3xTF32, M = 128,
 //               N = 128 pool entries per pass, accumulator in TMEM); epilogue
 //               score = ‖e‖² − 2 q'·e (L2) or −q'·e (IP) → global scratch.
-//   k_fes_select : one warp per query keeps the E smallest (score, id) keys
+//   k_fes_select4 / k_fes_select3 (cells > 8192 entries) : one warp per query keeps the E smallest (score, id) keys
 //               (Q10: the GEMM form is used for SELECTION only; stage ①
 //               recomputes direct-form δ).  Splitting the selection out keeps
 //               32+ warps per SM on it instead of the 4 epilogue warps of a tile.
@@ -107,118 +107,6 @@ struct FesParams {
     bool fold_norm;              // pool_img carries ‖e‖² in K column dps (A has 1 there): acc = score
 };
 
-// Grouped GEMM: one CTA per (cell, 128 bucketed queries) tile; scores of the
-// tile against every pool entry of the cell → global scratch (row = bucketed
-// position).  A = routed q' rows (hi/lo, resident for the tile), B = 128 pool
-// rows per pass; epilogue = tcgen05.ld + ‖e‖² − 2·acc (L2) / −acc (IP).
-template <int METRIC>
-__global__ void __launch_bounds__(kThreads, 1) k_fes_scores(FesParams p) {
-    extern __shared__ __align__(1024) unsigned char smem[];
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int t = blockIdx.x;
-    if (t >= p.toff[p.r]) return;
-    int c = 0;
-    while (c + 1 < p.r && p.toff[c + 1] <= t) ++c;
-    const int pos0 = p.qoff[c] + (t - p.toff[c]) * kM;
-    const int nrows = min(kM, p.qoff[c + 1] - pos0);
-    const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
-    const int kch = p.kchunks;
-
-    unsigned char* a_hi = smem;                               // kch × 16 KB
-    unsigned char* a_lo = a_hi + kch * 16384;
-    unsigned char* b_hi = a_lo + kch * 16384;                 // 16 KB
-    unsigned char* b_lo = b_hi + 16384;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(b_lo + 16384);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
-
-    if (warp == 0) tmem_alloc(tslot, kN);
-    if (tid == 0) mbar_init(bar, 1);
-    {
-        const int q = tid < nrows ? p.perm[pos0 + tid] : -1;
-        for (int kc = 0; kc < kch; ++kc) {
-#pragma unroll 8
-            for (int k = 0; k < 32; ++k) {
-                const int col = kc * 32 + k;
-                const float a = (q >= 0 && col < p.dps) ? __ldg(p.qp + (int64_t)q * p.dps + col) : 0.f;
-                float hi, lo;
-                split_tf32(a, hi, lo);
-                const uint32_t off = (uint32_t)kc * 16384 + sw128_off(tid, k);
-                *reinterpret_cast<float*>(a_hi + off) = hi;
-                *reinterpret_cast<float*>(a_lo + off) = lo;
-            }
-        }
-    }
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    const uint32_t tmem = *tslot;
-    const uint32_t idesc = make_idesc_tf32(kM, kN);
-    uint32_t phase = 0;
-    const int row = tid;                                      // TMEM lane = tile row
-    float* srow = p.scores + (int64_t)(pos0 + row) * p.sstride;
-
-    for (int n0 = 0; n0 < nc; n0 += kN) {
-        for (int kc = 0; kc < kch; ++kc) {
-            for (int idx = tid; idx < kN * 32; idx += kThreads) {
-                const int n = idx >> 5, k = idx & 31;
-                const int col = kc * 32 + k;
-                const float b = (n0 + n < nc && col < p.dps) ? __ldg(p.pool_vec + (int64_t)(pb + n0 + n) * p.dps + col) : 0.f;
-                float hi, lo;
-                split_tf32(b, hi, lo);
-                const uint32_t off = sw128_off(n, k);
-                *reinterpret_cast<float*>(b_hi + off) = hi;
-                *reinterpret_cast<float*>(b_lo + off) = lo;
-            }
-            fence_proxy_async();
-            tmem_fence_before();
-            __syncthreads();
-            if (tid == 0) {
-                tmem_fence_after();
-                const uint32_t sah = smem_u32(a_hi) + kc * 16384, sal = smem_u32(a_lo) + kc * 16384;
-                const uint32_t sbh = smem_u32(b_hi), sbl = smem_u32(b_lo);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint32_t ko = kk * 32;
-                    const uint32_t acc0 = (kc > 0 || kk > 0) ? 1u : 0u;
-                    mma_tf32(tmem, make_desc_sw128(sah + ko), make_desc_sw128(sbh + ko), idesc, acc0);
-                    mma_tf32(tmem, make_desc_sw128(sah + ko), make_desc_sw128(sbl + ko), idesc, 1u);
-                    mma_tf32(tmem, make_desc_sw128(sal + ko), make_desc_sw128(sbh + ko), idesc, 1u);
-                }
-                mma_commit(bar);
-            }
-            __syncwarp();
-            mbar_wait(bar, phase);
-            phase ^= 1;
-        }
-        tmem_fence_after();
-        for (int c0 = 0; c0 < kN; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-            const int jb = n0 + c0;
-            if (row < nrows && jb < nc) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    float4 o;
-                    float* op = &o.x;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int jj = jb + j + u;
-                        const float sc = METRIC == 0 ? fmaf(-2.f, v[j + u], jj < nc ? __ldg(p.pool_norm + pb + jj) : 0.f)
-                                                     : -v[j + u];
-                        op[u] = sc;
-                    }
-                    if (jb + j < nc) *reinterpret_cast<float4*>(srow + jb + j) = o;
-                }
-            }
-        }
-    }
-    tmem_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tmem_fence_after();
-        tmem_dealloc(tmem, kN);
-    }
-}
 
 // Same GEMM, warp-specialised and pipelined: warp 4 (one elected thread) streams
 // the cell's pre-split, pre-swizzled pool tiles with 1-D TMA bulk copies into a
@@ -373,48 +261,6 @@ size_t fes_scores_tma_smem(int kch) {
     return (size_t)kch * 2 * 16384 + 2 * 32768 + 8 * 8 + 16 + 512 + 4 * 32 * 36 * 4;
 }
 
-// Selection: one warp per bucketed query — E smallest (score, pool id) keys over
-// its cell's scores, kept sorted by the same threshold filter + rank merge as
-// the traversal (common.cuh).
-template <int SMAX>
-__global__ void __launch_bounds__(128) k_fes_select(FesParams p, int64_t m) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int E = p.E;
-    uint64_t* C = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)w * E;
-    const int64_t nwarps = (int64_t)gridDim.x * 4;
-    for (int64_t pos = (int64_t)blockIdx.x * 4 + w; pos < m; pos += nwarps) {
-        int c = 0;
-        while (c + 1 < p.r && p.qoff[c + 1] <= pos) ++c;
-        const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
-        const float* srow = p.scores + pos * p.sstride;
-        const int32_t* prow = p.pool_ids + pb;
-        int csz = 0;
-        // software-pipelined: the next batch's scores and ids are loaded before the
-        // current batch is filtered / merged
-        float ns = lane < nc ? srow[lane] : 0.f;
-        int32_t ni = lane < nc ? __ldg(prow + lane) : 0;
-        for (int j0 = 0; j0 < nc; j0 += 32) {
-            const int j = j0 + lane;
-            const float sc = ns;
-            const int32_t id = ni;
-            if (j + 32 < nc) {
-                ns = srow[j + 32];
-                ni = __ldg(prow + j + 32);
-            }
-            const uint64_t key = j < nc ? make_key(sc, id) : kKeyInf;
-            const uint64_t thresh = csz == E ? C[E - 1] : kKeyInf;
-            const bool pass = key < thresh;
-            const unsigned pbal = __ballot_sync(kFull, pass);
-            if (pbal == 0) continue;
-            int minr;
-            csz = rank_merge<SMAX>(C, csz, E, key, pass, pbal, lane, minr);
-        }
-        const int32_t q = p.perm[pos];
-        for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < csz ? key_id(C[j]) : -1;
-        __syncwarp();
-    }
-}
 
 // Selection, two passes (far fewer instructions than merging every passing key):
 //   1. every lane keeps the KP = ceil(E/32) smallest keys of its strided share in
@@ -474,114 +320,6 @@ __device__ __forceinline__ void warp_bitonic_regs(uint64_t (&t)[K], int lane) {
     }
 }
 
-template <int KPMAX, int SMAX>
-__global__ void __launch_bounds__(128) k_fes_select2(FesParams p, int64_t m) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int E = p.E, KP = (E + 31) / 32;
-    uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)w * kSelCap;
-    const int64_t nwarps = (int64_t)gridDim.x * 4;
-    for (int64_t pos = (int64_t)blockIdx.x * 4 + w; pos < m; pos += nwarps) {
-        int c = 0;
-        while (c + 1 < p.r && p.qoff[c + 1] <= pos) ++c;
-        const int pb = p.cell_off[c], nc = p.cell_off[c + 1] - pb;
-        const float* srow = p.scores + pos * p.sstride;
-        const int32_t* prow = p.pool_ids + pb;
-        const int32_t q = p.perm[pos];
-        // ---- pass 1: per-lane KP smallest keys
-        uint64_t t[KPMAX];
-#pragma unroll
-        for (int i = 0; i < KPMAX; ++i) t[i] = kKeyInf;
-        for (int j0 = 0; j0 < nc; j0 += 128) {              // 4 loads in flight per lane
-            float sv[4];
-            int32_t iv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = j0 + u * 32 + lane;
-                sv[u] = j < nc ? srow[j] : 0.f;
-                iv[u] = j < nc ? __ldg(prow + j) : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (j0 + u * 32 + lane >= nc) continue;
-                const uint64_t key = make_key(sv[u], iv[u]);
-                if (key < t[KP - 1]) {
-                    uint64_t x = key;
-#pragma unroll
-                    for (int i = 0; i < KPMAX; ++i) {
-                        if (i < KP && x < t[i]) { const uint64_t y = t[i]; t[i] = x; x = y; }
-                    }
-                }
-            }
-        }
-        // bitwise search for T = high word of the E-th smallest candidate
-        uint32_t T = 0xffffffffu;
-        if (nc > E) {
-            uint32_t lo = 0;                           // build T bit by bit: largest T with count(< T) < E
-            for (int b = 31; b >= 0; --b) {
-                const uint32_t trial = lo | (1u << b);
-                int cnt = 0;
-#pragma unroll
-                for (int i = 0; i < KPMAX; ++i) cnt += (i < KP && (uint32_t)(t[i] >> 32) < trial) ? 1 : 0;
-                cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
-                if (cnt < E) lo = trial;
-            }
-            T = lo;                                    // count(word < T) < E ≤ count(word ≤ T)
-        }
-        // ---- pass 2: compact all keys with distance word ≤ T, sort once
-        int M = 0;
-        bool overflow = false;
-        for (int j0 = 0; j0 < nc && !overflow; j0 += 32) {
-            const int j = j0 + lane;
-            uint64_t key = kKeyInf;
-            bool in = false;
-            if (j < nc) {
-                key = make_key(srow[j], __ldg(prow + j));
-                in = (uint32_t)(key >> 32) <= T;
-            }
-            const unsigned bal = __ballot_sync(kFull, in);
-            const int add = __popc(bal);
-            if (M + add > kSelCap) { overflow = true; break; }
-            if (in) buf[M + __popc(bal & ((1u << lane) - 1u))] = key;
-            M += add;
-        }
-        __syncwarp();
-        if (!overflow && M <= 128) {                  // common case: sort in registers
-            uint64_t t4[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) t4[a] = a * 32 + lane < M ? buf[a * 32 + lane] : kKeyInf;
-            warp_bitonic_regs<4>(t4, lane);
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int j = a * 32 + lane;
-                if (j < E) p.entries[(int64_t)q * E + j] = j < M ? key_id(t4[a]) : -1;
-            }
-            for (int j = 128 + lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = -1;
-        } else if (!overflow) {
-            int n2 = 32;
-            while (n2 < M) n2 <<= 1;
-            for (int i = M + lane; i < n2; i += 32) buf[i] = kKeyInf;
-            __syncwarp();
-            warp_bitonic_smem(buf, n2, lane);
-            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < M ? key_id(buf[j]) : -1;
-        } else {                                       // heavy ties: merge path
-            uint64_t* C = buf;
-            int csz = 0;
-            for (int j0 = 0; j0 < nc; j0 += 32) {
-                const int j = j0 + lane;
-                const uint64_t key = j < nc ? make_key(srow[j], __ldg(prow + j)) : kKeyInf;
-                const uint64_t thresh = csz == E ? C[E - 1] : kKeyInf;
-                const bool pass = key < thresh;
-                const unsigned pbal = __ballot_sync(kFull, pass);
-                if (pbal == 0) continue;
-                int minr;
-                csz = rank_merge<SMAX>(C, csz, E, key, pass, pbal, lane, minr);
-            }
-            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < csz ? key_id(C[j]) : -1;
-        }
-        __syncwarp();
-    }
-}
 
 // Same two-pass selection, latency-restructured (one warp per query):
 //   * the routed cell is found lane-parallel (one ballot over qoff per 32 cells),
@@ -592,7 +330,7 @@ __global__ void __launch_bounds__(128) k_fes_select2(FesParams p, int64_t m) {
 //     warp prefix sum and loads the pool ids of the selected entries only,
 //   * ≤ 128 candidates are sorted in registers; larger sets take the smem sort,
 //     more than kSelCap (heavy ties) the rank-merge fallback.
-// Keys and hence entries are identical to k_fes_select / k_fes_select2.
+// Keys and hence entries are identical to k_fes_select4's.
 #ifndef PA_SEL_MINB
 #define PA_SEL_MINB 6
 #endif
@@ -648,7 +386,7 @@ __global__ void __launch_bounds__(128, PA_SEL_MINB) k_fes_select3(FesParams p, i
         }
         uint32_t T = 0xffffffffu;
         if (nc > E) {
-            uint32_t lo = 0;                              // largest T with count(< T) < E (see k_fes_select2)
+            uint32_t lo = 0;                              // largest T with count(< T) < E
             for (int b = 31; b >= 0; --b) {
                 const uint32_t trial = lo | (1u << b);
                 int cnt = 0;
@@ -913,7 +651,7 @@ __global__ void __launch_bounds__(128, 4) k_fes_select4(FesParams p, int64_t m) 
     }
 }
 
-size_t fes_scores_smem(int kch) { return (size_t)kch * 2 * 16384 + 2 * 16384 + 16; }
+size_t fes_scores_smem(int kch) { return fes_scores_tma_smem(kch); }
 
 }  // namespace
 
@@ -937,42 +675,27 @@ int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
     p.pool_img = ix.pool_img; p.chunk_off = ix.chunk_off; p.fold_norm = ix.fes_fold_norm;
     const unsigned grid = (unsigned)((a.m + kM - 1) / kM + ix.fes_r);
     void* args[] = {&p};
-    const char* ke = std::getenv("PA_FES_SCORES");
-    if (ix.pool_img && !(ke && !std::strcmp(ke, "plain"))) {
+    {
         const size_t smem = fes_scores_tma_smem(p.kchunks);
         void* fn = ix.metric == 0 ? (void*)k_fes_scores_tma<0> : (void*)k_fes_scores_tma<1>;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaLaunchKernel(fn, dim3(grid), dim3(160), args, smem, s);
-    } else {
-        const size_t smem = fes_scores_smem(p.kchunks);
-        void* fn = ix.metric == 0 ? (void*)k_fes_scores<0> : (void*)k_fes_scores<1>;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
     }
-    const char* se = std::getenv("PA_FES_SELECT");
+    // selection: k_fes_select4 up to 8192-entry cells, k_fes_select3 above (same entries)
     void* sel;
-    size_t ssm;
-    if (se && !std::strcmp(se, "merge")) {
-        sel = a.E <= 64 ? (void*)k_fes_select<2> : a.E <= 128 ? (void*)k_fes_select<4> : (void*)k_fes_select<8>;
-        ssm = (size_t)4 * a.E * 8;
-    } else if (!(se && (!std::strcmp(se, "two-pass") || !std::strcmp(se, "select3"))) && ix.max_cell <= 2048 * 4) {
+    size_t ssm = (size_t)4 * kSelCap * 8;
+    if (ix.max_cell <= 2048 * 4) {
         const int SM = a.E <= 64 ? 2 : a.E <= 128 ? 4 : 8;
         const int G = ix.max_cell <= 2048 ? 1 : ix.max_cell <= 4096 ? 2 : 4;
         void* t[3][3] = {{(void*)k_fes_select4<2, 1>, (void*)k_fes_select4<2, 2>, (void*)k_fes_select4<2, 4>},
                          {(void*)k_fes_select4<4, 1>, (void*)k_fes_select4<4, 2>, (void*)k_fes_select4<4, 4>},
                          {(void*)k_fes_select4<8, 1>, (void*)k_fes_select4<8, 2>, (void*)k_fes_select4<8, 4>}};
         sel = t[SM == 2 ? 0 : SM == 4 ? 1 : 2][G == 1 ? 0 : G == 2 ? 1 : 2];
-        ssm = (size_t)4 * kSelCap * 8;
-    } else if (!(se && !std::strcmp(se, "two-pass"))) {
+    } else {
         constexpr int NV = PA_SEL_NV;
         sel = a.E <= 32 ? (void*)k_fes_select3<2, 2, NV> : a.E <= 64 ? (void*)k_fes_select3<4, 2, NV>
             : a.E <= 96 ? (void*)k_fes_select3<6, 4, NV> : a.E <= 128 ? (void*)k_fes_select3<8, 4, NV>
             : (void*)k_fes_select3<16, 8, NV>;
-        ssm = (size_t)4 * kSelCap * 8;
-    } else {
-        sel = a.E <= 64 ? (void*)k_fes_select2<2, 2> : a.E <= 96 ? (void*)k_fes_select2<3, 4>
-            : a.E <= 128 ? (void*)k_fes_select2<4, 4> : (void*)k_fes_select2<8, 8>;
-        ssm = (size_t)4 * kSelCap * 8;
     }
     cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     int64_t blocks = (a.m + 3) / 4;

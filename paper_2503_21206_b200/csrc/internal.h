@@ -49,6 +49,7 @@ struct SearchArgs {
     uint32_t flags = 0;
     int32_t hash_log2 = 12;
     int32_t bloom_log2 = 0;        // > 0: stage-① visited set = bloom filter, 3 segments × 2^this bits (NEXT-f1)
+    bool wide_visited = false;     // force the 32-bit exact visited table (pa_search_opts.check_path test hook)
     const float* q = nullptr;      // [m][dim]
     float* qp = nullptr;           // [m][rdim_pad]  projected q'
     float* qres = nullptr;         // [m][dim − rdim] (optional) residual projection for host stages

@@ -105,10 +105,6 @@ pa_status check_csr(const int64_t* off, const int32_t* nb, int64_t n, int32_t ma
 // 16-bit quotiented slots (ids < 2^24): 2^11 up to ef 64, 2^12 above (8 KB);
 // 32-bit slots: 2^11 up to ef 128 (8 KB), 2^12 above.
 int default_hash_log2(int ef, int64_t n) {
-    if (const char* e = std::getenv("PA_HASH_LOG2")) {
-        int v = std::atoi(e);
-        if (v >= 5 && v <= 15) return v;
-    }
     if (n <= (1 << 24)) return ef <= 64 ? 11 : 12;
     return ef <= 128 ? 11 : 12;
 }
@@ -218,7 +214,7 @@ pa_status ensure_spill(pa_index* ix, int64_t warps) {
 
 struct Resolved {
     int32_t stages, ef1, ef2, ef3, E, width, refine, hash_log2, threads, bloom_log2;
-    uint32_t flags;
+    uint32_t flags, check;
 };
 
 pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, int64_t n) {
@@ -236,6 +232,8 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, i
     r->width = o->width ? o->width : 1;
     r->refine = o->refine_iters == 0 ? 2 : (o->refine_iters < 0 ? 0 : o->refine_iters);
     r->flags = o->flags;
+    r->check = o->check_path;
+    if (r->check & ~(uint32_t)(PA_CHECK_SIMT | PA_CHECK_WIDE_VISITED)) return fail(PA_EINVAL, "bad check_path %u", r->check);
     r->hash_log2 = o->hash_slots_log2 ? o->hash_slots_log2 : default_hash_log2(r->ef1, n);
     r->threads = threads_default(o->host_threads);
     r->bloom_log2 = o->bloom_log2;
@@ -306,6 +304,7 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     pa::SearchArgs a;
     a.m = m; a.k = k; a.ef = r.ef1; a.E = r.E; a.flags = r.flags; a.hash_log2 = r.hash_log2;
     a.bloom_log2 = r.bloom_log2;
+    a.wide_visited = (r.check & PA_CHECK_WIDE_VISITED) != 0;
     if (a.bloom_log2 > 0 && dd.ell_w != 32) return fail(PA_ENOTSUP, "bloom visited set needs max_degree <= 32");
     a.q = d_q; a.qp = ix->qp + row0 * dd.rdim_pad;
     a.qres = want_qres ? ix->qres + row0 * std::max(1, dd.dim - dd.rdim) : nullptr;
@@ -336,8 +335,7 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
 
     int launches = 0;
     CU(cudaEventRecord(ix->ev[0], s));
-    const char* pe = std::getenv("PA_PROJECT");           // A/B and test hooks: "simt" selects the SIMT kernels
-    const bool force_simt = pe && !std::strcmp(pe, "simt");
+    const bool force_simt = (r.check & PA_CHECK_SIMT) != 0;   // test hook: the SIMT cross-check kernels
     if (!force_simt && pa::project_tc_supported(ix->dev, a.qres != nullptr)) {
         launches += pa::launch_project_tc(ix->dev, a, s);
         a.cell_ready = true;
@@ -346,9 +344,7 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     }
     CU(cudaGetLastError());
     CU(cudaEventRecord(ix->ev[1], s));
-    const char* fe = std::getenv("PA_FES");
-    const bool force_fes_simt = fe && !std::strcmp(fe, "simt");
-    if (a.cell_ready && !force_fes_simt && !(a.flags & PA_NO_FES) && pa::fes_tc_supported(ix->dev, a.E))
+    if (a.cell_ready && !force_simt && !(a.flags & PA_NO_FES) && pa::fes_tc_supported(ix->dev, a.E))
         launches += pa::launch_fes_tc(ix->dev, a, s);
     else
         launches += pa::launch_fes(ix->dev, a, s);

@@ -1,8 +1,5 @@
 // a5 + a6 launcher: picks the k_traverse variant (traverse_kernel.cuh,
 // instantiated in traverse_inst_*.cu) and sizes the persistent grid.
-#include <cstdlib>
-#include <cstring>
-
 #include "internal.h"
 
 namespace pa {
@@ -35,8 +32,7 @@ namespace {
 using trav::kTW;
 
 bool use_compact(const DevIndex& ix, const SearchArgs& a) {
-    const char* e = std::getenv("PA_VISITED");
-    if (e && !std::strcmp(e, "wide")) return false;
+    if (a.wide_visited) return false;
     return ix.n <= (1 << 24) && a.hash_log2 >= 11 && a.hash_log2 <= 13;
 }
 void* pick(const DevIndex& ix, const SearchArgs& a) {
@@ -48,8 +44,7 @@ void* pick(const DevIndex& ix, const SearchArgs& a) {
         if (ix.metric == 0) return h ? trav::traverse_pick_pipe_0bh(a.ef, d, tr) : trav::traverse_pick_pipe_0bf(a.ef, d, tr);
         return h ? trav::traverse_pick_pipe_1bh(a.ef, d, tr) : trav::traverse_pick_pipe_1bf(a.ef, d, tr);
     }
-    const char* ve = std::getenv("PA_TRAVERSE");
-    if (ix.ell_w == 32 && !(ve && !std::strcmp(ve, "v1"))) {        // software-pipelined kernel
+    if (ix.ell_w == 32) {                                            // software-pipelined kernel
         const bool h = ix.reduced_h != nullptr;
         const int d = h ? ix.rdim_h : ix.rdim_pad;
         if (ix.metric == 0) {
