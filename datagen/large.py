@@ -180,6 +180,8 @@ def knn_candidates(X: torch.Tensor, ids: torch.Tensor, lab: torch.Tensor, cent: 
             break
         for a0 in range(0, cnt_l[j], a_max):
             items.append((j, a0, min(a_max, cnt_l[j] - a0)))
+    # batch items of similar candidate-set size (the padded Lc dominates the GEMM and top-k work)
+    items.sort(key=lambda it: (-tot_l[it[0]], -it[2]))
     prof = _Prof()
     prof.tick("start")
     i = 0
@@ -372,6 +374,28 @@ def reverse_fill(X: torch.Tensor, ids: torch.Tensor, rows: torch.Tensor, R: int,
     return out
 
 
+def fill_free(rows: torch.Tensor, cand: torch.Tensor, R: int, chunk: int = 1 << 15) -> torch.Tensor:
+    """Slots still free after pruning and back-links take the nearest remaining
+    candidates (ascending), so every row has min(R, #distinct candidates) edges —
+    the diverse (occlusion-selected) edges and the back-links first, then the
+    closest of the occluded ones, as HNSW implementations that keep pruned
+    connections do.  rows [n][R], cand [n][L] int32 (−1 pad) → rows."""
+    n, L = cand.shape
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        r = rows[s:e]
+        c = cand[s:e]
+        present = (c[:, :, None] == r[:, None, :]).any(2)
+        elig = (c >= 0) & ~present
+        deg = (r >= 0).sum(1, keepdim=True)
+        rank = torch.cumsum(elig.to(torch.int64), 1)
+        take = elig & (deg + rank <= R)
+        bi, li = torch.nonzero(take, as_tuple=True)
+        slot = (deg[bi, 0] + rank[bi, li] - 1)
+        r[bi, slot] = c[bi, li]
+    return rows
+
+
 def build_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor], seed: int, P: int = 0,
                 part_size: int = 1000, slack: int = 16, labels: Optional[torch.Tensor] = None) -> torch.Tensor:
     """The graph tool at scale (same three steps as `datagen.build_graph`):
@@ -411,11 +435,18 @@ def build_graph(X: torch.Tensor, R: int, ids: Optional[torch.Tensor], seed: int,
         _log(f"graph n={n}: refine pass {time.time() - t:.1f}s")
     t = time.time()
     rows = prune(X, ids, cand, R, 2 * R, alpha=float(os.environ.get("PA_GRAPH_ALPHA", "1.0")))
-    del cand
+    fill = os.environ.get("PA_GRAPH_FILL", "1") == "1"
+    if not fill:
+        del cand
     _log(f"graph n={n}: prune {time.time() - t:.1f}s")
     t = time.time()
     rows = reverse_fill(X, ids, rows, R, X.shape[0])
     _log(f"graph n={n}: reverse fill {time.time() - t:.1f}s")
+    if fill:
+        t = time.time()
+        rows = fill_free(rows, cand, R)
+        del cand
+        _log(f"graph n={n}: nearest-candidate fill {time.time() - t:.1f}s")
     return rows
 
 

@@ -110,7 +110,10 @@ typedef struct {
     int32_t stages;          /* pa_stages (0 ⇒ PA_STAGES_GPU)                                 */
     int32_t ef1, ef2, ef3;   /* per-stage candidate capacities, ≤ 256                          */
     int32_t entries;         /* E entries seeded into C per query (Q8)                          */
-    int32_t width;           /* must be 1 on the GPU (PA_ENOTSUP otherwise)                     */
+    int32_t width;           /* search width w, 1..8 (SURVEY §8.c O6 generalisation of Alg 1: the w
+                                smallest unchecked entries are expanded per iteration, rows visited in
+                                key order; all three stages).  w > 1 runs the sequential kernel with
+                                the exact visited set (PA_ENOTSUP with bloom_log2 > 0)            */
     int32_t refine_iters;    /* stage-② expansions (−1 ⇒ 0 iterations; 0 ⇒ default 2)          */
     uint32_t flags;          /* PA_NO_* ablation toggles                                       */
     int32_t hash_slots_log2; /* visited-hash smem slots = 2^this (0 ⇒ auto); test hook for spill */

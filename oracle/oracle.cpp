@@ -307,6 +307,7 @@ void search_one(const OrcIndex& ix, const float* q, const OrcOpts& o, const OrcO
         // ---- O9 stage ③ final traversal on the full graph (Q23)
         std::vector<Cand> C3 = C2;
         for (Cand& c : C3) c.checked = false;                  // carry entries start unchecked
+        if ((int32_t)C3.size() > o.ef3) C3.resize(o.ef3);      // capacity ef3 from the start (as O5's resize(ef1))
         greedy(ix.full_offsets, ix.full_neighbors, dfull, o.ef3, o.width, -1, C3, vis2,
                local[kNExp3], local[kNDist3], nullptr);
         result = C3;

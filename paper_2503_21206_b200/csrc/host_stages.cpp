@@ -83,36 +83,42 @@ inline float dist_full(const float* __restrict__ q, const float* __restrict__ x,
 }
 
 // Alg 1 with a sorted array C; `max_iters` < 0 ⇒ until no unchecked.
+// Width w: each iteration marks the w smallest unchecked entries
+// checked and visits their rows in key order; inserting the new keys one at a
+// time with truncation to ef leaves the same C as merging them all and then
+// resizing (truncation only drops keys that cannot be among the ef smallest).
 template <class DistFn, class PrefetchFn>
-void greedy(const int64_t* off, const int32_t* nb, DistFn dist, PrefetchFn prefetch, int ef, long max_iters,
+void greedy(const int64_t* off, const int32_t* nb, DistFn dist, PrefetchFn prefetch, int ef, int w, long max_iters,
             std::vector<Cand>& C, VisitedSet& vis, int64_t& n_dist) {
     long it = 0;
+    int32_t us[64];
     while (max_iters < 0 || it < max_iters) {
-        int p = -1;
-        for (size_t i = 0; i < C.size(); ++i)
-            if (!C[i].checked) { p = (int)i; break; }
-        if (p < 0) break;
+        int nu = 0;
+        for (size_t i = 0; i < C.size() && nu < w; ++i)
+            if (!C[i].checked) { C[i].checked = true; us[nu++] = C[i].id; }
+        if (nu == 0) break;
         ++it;
-        C[p].checked = true;
-        const int32_t u = C[p].id;
-        // unvisited neighbours first (stored order), their rows prefetched, then distances
-        int32_t fresh[64];
-        for (int64_t e0 = off[u]; e0 < off[u + 1];) {
-            int nf = 0;
-            for (; e0 < off[u + 1] && nf < 64; ++e0) {
-                const int32_t v = nb[e0];
-                if (!vis.insert(v)) continue;
-                fresh[nf++] = v;
-                prefetch(v);
-            }
-            for (int i = 0; i < nf; ++i) {
-                const int32_t v = fresh[i];
-                ++n_dist;
-                Cand c{dist(v), v, false};
-                if ((int)C.size() == ef && !key_less(c, C.back())) continue;
-                auto pos = std::lower_bound(C.begin(), C.end(), c, key_less);
-                C.insert(pos, c);
-                if ((int)C.size() > ef) C.pop_back();
+        for (int x = 0; x < nu; ++x) {
+            const int32_t u = us[x];
+            // unvisited neighbours first (stored order), their rows prefetched, then distances
+            int32_t fresh[64];
+            for (int64_t e0 = off[u]; e0 < off[u + 1];) {
+                int nf = 0;
+                for (; e0 < off[u + 1] && nf < 64; ++e0) {
+                    const int32_t v = nb[e0];
+                    if (!vis.insert(v)) continue;
+                    fresh[nf++] = v;
+                    prefetch(v);
+                }
+                for (int i = 0; i < nf; ++i) {
+                    const int32_t v = fresh[i];
+                    ++n_dist;
+                    Cand c{dist(v), v, false};
+                    if ((int)C.size() == ef && !key_less(c, C.back())) continue;
+                    auto pos = std::lower_bound(C.begin(), C.end(), c, key_less);
+                    C.insert(pos, c);
+                    if ((int)C.size() > ef) C.pop_back();
+                }
             }
         }
     }
@@ -167,14 +173,14 @@ void run_host_stages(const HostStageArgs& a) {
                 if ((int)C.size() > a.ef3) C.resize(a.ef3);
             } else {
                 if ((int)C.size() > a.ef2) C.resize(a.ef2);
-                greedy(a.sub.off, a.sub.nb, dfull, pref, a.ef2, a.refine_iters, C, vis, my2);
+                greedy(a.sub.off, a.sub.nb, dfull, pref, a.ef2, a.width, a.refine_iters, C, vis, my2);
             }
             // ---- stage ③: Alg 1 on the full graph, carry entries unchecked, visited kept (Q23)
             // ef2 > ef3: keep the ef3 smallest now — the same set Alg 1's resize (l.11)
             // leaves after the first expansion, whose node is C[0] either way.
             if ((int)C.size() > a.ef3) C.resize(a.ef3);
             for (Cand& c : C) c.checked = false;
-            greedy(a.full.off, a.full.nb, dfull, pref, a.ef3, -1, C, vis, my3);
+            greedy(a.full.off, a.full.nb, dfull, pref, a.ef3, a.width, -1, C, vis, my3);
             for (int j = 0; j < a.k; ++j) {
                 const bool ok = j < (int)C.size();
                 a.out_ids[q * a.k + j] = ok ? C[j].id : -1;

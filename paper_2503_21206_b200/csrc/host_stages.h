@@ -16,6 +16,7 @@ struct HostStageArgs {
     int64_t m = 0;
     int32_t k = 10, ef1 = 64, ef2 = 32, ef3 = 64;
     long refine_iters = 2;
+    int32_t width = 1;                  // search width w: expansions per Alg 1 iteration
     uint32_t flags = 0;
     int threads = 0;
     const int32_t* cand_ids = nullptr;  // [m][ef1] stage-① C

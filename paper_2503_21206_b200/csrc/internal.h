@@ -49,7 +49,8 @@ struct SearchArgs {
     uint32_t flags = 0;
     int32_t hash_log2 = 12;
     int32_t bloom_log2 = 0;        // > 0: stage-① visited set = bloom filter, 3 segments × 2^this bits (NEXT-f1)
-    bool wide_visited = false;     // force the 32-bit exact visited table (pa_search_opts.check_path test hook)
+    bool wide_visited = false;
+    int32_t width = 1;             // search width w (1 = Alg 1; > 1: the sequential kernel, exact visited set)     // force the 32-bit exact visited table (pa_search_opts.check_path test hook)
     const float* q = nullptr;      // [m][dim]
     float* qp = nullptr;           // [m][rdim_pad]  projected q'
     float* qres = nullptr;         // [m][dim − rdim] (optional) residual projection for host stages
@@ -81,7 +82,7 @@ struct SearchArgs {
 // Stages ②③ on the GPU (NEXT-f3, k_refine).
 struct Refine23 {
     int64_t m = 0;
-    int32_t k = 10, ef1 = 64, ef2 = 32, ef3 = 64, refine_iters = 2;
+    int32_t k = 10, ef1 = 64, ef2 = 32, ef3 = 64, refine_iters = 2, width = 1;
     uint32_t flags = 0;
     int32_t D = 0, dp = 0, qlen = 0, qp_stride = 0;
     const float* qp = nullptr;          // [m][qp_stride] q'

@@ -243,7 +243,9 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, i
     if (r->ef1 < 1 || r->ef2 < 1 || r->ef3 < 1 || r->E < 1 || r->E > 1024) return fail(PA_EINVAL, "bad ef/entries");
     if (r->stages == PA_STAGES_GPU && k > r->ef1) return fail(PA_EINVAL, "k = %d > ef1 = %d", k, r->ef1);
     if (r->stages != PA_STAGES_GPU && (k > r->ef3 || k > r->ef2)) return fail(PA_EINVAL, "k > ef2/ef3");
-    if (r->width != 1) return fail(PA_ENOTSUP, "search width w = %d: only w = 1 on the GPU", r->width);
+    if (r->width < 1 || r->width > 8) return fail(PA_EINVAL, "search width w = %d not in 1..8", r->width);
+    if (r->width > 1 && r->bloom_log2 > 0)
+        return fail(PA_ENOTSUP, "search width w > 1 uses the exact visited set (bloom_log2 must be 0)");
     if (r->hash_log2 < 5 || r->hash_log2 > 15) return fail(PA_EINVAL, "hash_slots_log2 = %d", r->hash_log2);
     return PA_OK;
 }
@@ -305,6 +307,7 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     a.m = m; a.k = k; a.ef = r.ef1; a.E = r.E; a.flags = r.flags; a.hash_log2 = r.hash_log2;
     a.bloom_log2 = r.bloom_log2;
     a.wide_visited = (r.check & PA_CHECK_WIDE_VISITED) != 0;
+    a.width = r.width;
     if (a.bloom_log2 > 0 && dd.ell_w != 32) return fail(PA_ENOTSUP, "bloom visited set needs max_degree <= 32");
     a.q = d_q; a.qp = ix->qp + row0 * dd.rdim_pad;
     a.qres = want_qres ? ix->qres + row0 * std::max(1, dd.dim - dd.rdim) : nullptr;
@@ -356,6 +359,7 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     if (r.stages == PA_STAGES_FULL_GPU) {                   // NEXT-f3: ②③ on the GPU
         pa::Refine23 f;
         f.m = m; f.k = k; f.ef1 = r.ef1; f.ef2 = r.ef2; f.ef3 = r.ef3; f.refine_iters = r.refine; f.flags = r.flags;
+        f.width = r.width;
         f.D = dd.dim; f.dp = dd.rdim; f.qlen = (dd.dim + 3) & ~3; f.qp = a.qp; f.qp_stride = dd.rdim_pad;
         f.qres = a.qres; f.cand = a.cand_ids;
         f.sub_ell = dd.ell; f.sub_w = dd.ell_w; f.full_ell = dd.full_ell; f.full_w = dd.full_w;
@@ -888,7 +892,7 @@ static pa_status search_host_impl(pa_index* ix, const float* queries, int64_t m,
         h.sub.off = ix->h_sub_off.data(); h.sub.nb = ix->h_sub_nb.data();
         h.full.off = ix->h_full_off; h.full.nb = ix->h_full_nb;
         h.rotated = ix->h_rotated;
-        h.m = m; h.k = k; h.ef1 = r.ef1; h.ef2 = r.ef2; h.ef3 = r.ef3; h.refine_iters = r.refine;
+        h.m = m; h.k = k; h.ef1 = r.ef1; h.ef2 = r.ef2; h.ef3 = r.ef3; h.refine_iters = r.refine; h.width = r.width;
         h.flags = r.flags; h.threads = r.threads;
         h.cand_ids = ix->h_cand_ids; h.cand_d = ix->h_cand_d; h.qp = ix->h_qp; h.qp_stride = d.rdim_pad;
         h.qres = ix->h_qres; h.out_ids = out_ids; h.out_d = out_d;

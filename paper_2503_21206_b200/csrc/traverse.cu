@@ -38,13 +38,13 @@ bool use_compact(const DevIndex& ix, const SearchArgs& a) {
 void* pick(const DevIndex& ix, const SearchArgs& a) {
     const bool cp = use_compact(ix, a), tr = a.trace_cap > 0;
     if (a.bloom_log2 > 0) {                                          // bloom visited set: pipelined kernel only
-        if (ix.ell_w != 32) return nullptr;
+        if (ix.ell_w != 32 || a.width > 1) return nullptr;
         const bool h = ix.reduced_h != nullptr;
         const int d = h ? ix.rdim_h : ix.rdim_pad;
         if (ix.metric == 0) return h ? trav::traverse_pick_pipe_0bh(a.ef, d, tr) : trav::traverse_pick_pipe_0bf(a.ef, d, tr);
         return h ? trav::traverse_pick_pipe_1bh(a.ef, d, tr) : trav::traverse_pick_pipe_1bf(a.ef, d, tr);
     }
-    if (ix.ell_w == 32) {                                            // software-pipelined kernel
+    if (ix.ell_w == 32 && a.width == 1) {                            // software-pipelined kernel
         const bool h = ix.reduced_h != nullptr;
         const int d = h ? ix.rdim_h : ix.rdim_pad;
         if (ix.metric == 0) {

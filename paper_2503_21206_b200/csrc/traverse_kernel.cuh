@@ -39,6 +39,7 @@ constexpr int kTW = 4;                 // warps per block
 #define PA_TRAV_MINB_BLOOM 8           // same, bloom visited set (3 KB of smem per warp instead of 8 KB)
 #endif
 constexpr int kIterCap = 1000000;      // Q16 safety cap (status 2)
+constexpr int kMaxWidth = 8;           // search width w ≤ 8 on the GPU
 #ifndef PA_GROUP_L32
 #define PA_GROUP_L32 4                 // lanes per row in the distance gathers, fp32 rows
 #endif
@@ -259,6 +260,42 @@ __global__ void __launch_bounds__(kTW * 32, PA_TRAV_MINB) k_traverse(DevIndex ix
         int32_t sv[2] = {-1, -1};
         if (!(a.flags & 4u)) {
             for (int it = 0; status == 0; ++it) {
+                if (a.width > 1) {
+                    // Search width w: the w smallest unchecked keys are
+                    // marked checked together and their rows visited in key order; merging
+                    // row by row with truncation leaves the same C as one merge + resize.
+                    int ps[kMaxWidth];
+                    int nu = 0;
+                    for (int t = hint >> 5; t * 32 < csz && nu < a.width; ++t) {
+                        const int i = t * 32 + lane;
+                        unsigned b = __ballot_sync(kFull, i < csz && !key_checked(C[i]));
+#pragma unroll
+                        for (int x = 0; x < kMaxWidth; ++x)
+                            if (b && nu < a.width) { ps[nu++] = t * 32 + __ffs(b) - 1; b &= b - 1; }
+                    }
+                    if (nu == 0) break;                                 // l.12: no unchecked node
+                    int32_t us[kMaxWidth];
+#pragma unroll
+                    for (int x = 0; x < kMaxWidth; ++x) us[x] = x < nu ? key_id(C[ps[x]]) : -1;
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int x = 0; x < nu; ++x) C[ps[x]] |= 1ull;
+                    hint = ps[nu - 1] + 1;
+                    __syncwarp();
+#pragma unroll
+                    for (int x = 0; x < kMaxWidth; ++x) {
+                        if (x >= nu || status != 0) break;
+                        if (TRACE && lane == 0 && n_exp < a.trace_cap) a.trace_expand[q * a.trace_cap + n_exp] = us[x];
+                        ++n_exp;
+                        for (int c = 0; c < NCH && status == 0; ++c) {
+                            const int32_t v = __ldg(ix.ell + (int64_t)us[x] * ELLW + c * 32 + lane);
+                            const bool isnew = visit_batch(v);
+                            if (status == 0) merge_batch(v, isnew, [] {});
+                        }
+                    }
+                    if (it >= kIterCap) status = 2;
+                    continue;
+                }
                 int p = -1, p2 = -1;
                 for (int t = hint >> 5; t * 32 < csz; ++t) {
                     const int i = t * 32 + lane;
@@ -728,6 +765,34 @@ __global__ void __launch_bounds__(kTW * 32, PA_REFINE_MINB) k_refine(Refine23 a)
         auto expand = [&](const int32_t* ell, int ellw, int max_it) {
             int32_t spec_u = -1, sv0 = -1, sv1 = -1;
             for (int it = 0; status == 0 && (max_it < 0 || it < max_it); ++it) {
+                if (a.width > 1) {                               // search width w (O6), as in k_traverse
+                    int ps[kMaxWidth];
+                    int nu = 0;
+                    for (int t = hint >> 5; t * 32 < csz && nu < a.width; ++t) {
+                        const int i = t * 32 + lane;
+                        unsigned b = __ballot_sync(kFull, i < csz && !key_checked(C[i]));
+#pragma unroll
+                        for (int x = 0; x < kMaxWidth; ++x)
+                            if (b && nu < a.width) { ps[nu++] = t * 32 + __ffs(b) - 1; b &= b - 1; }
+                    }
+                    if (nu == 0) break;
+                    int32_t us[kMaxWidth];
+#pragma unroll
+                    for (int x = 0; x < kMaxWidth; ++x) us[x] = x < nu ? key_id(C[ps[x]]) : -1;
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int x = 0; x < nu; ++x) C[ps[x]] |= 1ull;
+                    hint = ps[nu - 1] + 1;
+                    __syncwarp();
+#pragma unroll
+                    for (int x = 0; x < kMaxWidth; ++x) {
+                        if (x >= nu || status != 0) break;
+                        step(__ldg(ell + (int64_t)us[x] * ellw + lane), false);
+                        if (ellw > 32 && status == 0) step(__ldg(ell + (int64_t)us[x] * ellw + 32 + lane), false);
+                    }
+                    if (it >= kIterCap) status = 2;
+                    continue;
+                }
                 int p = -1, p2 = -1;
                 for (int t = hint >> 5; t * 32 < csz; ++t) {
                     const int i = t * 32 + lane;

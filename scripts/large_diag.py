@@ -24,14 +24,20 @@ m = q.shape[0]
 oi = torch.empty(m, 10, dtype=torch.int32, device="cuda")
 od = torch.empty(m, 10, dtype=torch.float32, device="cuda")
 rec = lambda ids, gt: sum(len(set(a) & set(b)) for a, b in zip(ids[:, :10].tolist(), gt[:, :10].tolist())) / (10 * len(ids))
-for ef in (64, 128, 256):
-    for fl in (0, pa.PA_NO_FES):
-        ix.search_device(q, 10, ef, oi, od, bloom_log2=12, flags=fl)
+for ef in (64, 96, 128, 160, 192, 256):
+    for bl in (0, 12, 13, 14):
+        try:
+            ix.search_device(q, 10, ef, oi, od, bloom_log2=bl)
+        except pa.PAError as e:
+            print(f"GPU ef={ef} bloom={bl}: {e}", flush=True)
+            continue
         torch.cuda.synchronize()
         st = ix.stats()
-        print(f"GPU ef={ef} flags={fl} GT_sub {rec(oi.cpu().numpy(), inst['gt_sub_ids']):.4f} trav {st['ms_traverse']:.3f} ms "
-              f"n_dist/q {st['sum_n_dist'] / m:.0f}", flush=True)
+        print(f"GPU ef={ef} bloom={bl} GT_sub {rec(oi.cpu().numpy(), inst['gt_sub_ids']):.4f} trav {st['ms_traverse']:.3f} ms "
+              f"gpu {st['ms_total_gpu']:.3f} ms n_dist/q {st['sum_n_dist'] / m:.0f} n_exp/q {st['sum_n_exp'] / m:.0f}", flush=True)
 ix.close()
+if os.environ.get("DIAG_ORACLE", "1") != "1":
+    sys.exit(0)
 # oracle, perfect entry: one query at a time with pool = [GT_sub top-1]
 sel = np.arange(0, m, m // 40)[:40]
 for ef in (64, 256, 1024):

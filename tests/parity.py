@@ -41,7 +41,9 @@ def _tol(d, qn2, ipscale=None):
     return REL * (ipscale + d) + 1e-30
 
 
-def compare(inst, gpu: dict, ref: dict, k: int, ef: int, gt_ids=None, check_traces=True) -> ParityReport:
+def compare(inst, gpu: dict, ref: dict, k: int, ef: int, gt_ids=None, check_traces=True, width: int = 1) -> ParityReport:
+    """width w > 1: an iteration expands the w best unchecked keys, so a first
+    differing expansion is explained by a near-tie with any of them."""
     metric = inst.get("metric", "l2")
     Qh = orc.project(inst["queries"], inst["basis"])
     dp = inst["reduced"].shape[1]
@@ -171,7 +173,7 @@ def compare(inst, gpu: dict, ref: dict, k: int, ef: int, gt_ids=None, check_trac
                 abs(du - Kd[ef - 1]) <= tol(q, [u], np.array([max(abs(du), abs(Kd[ef - 1]))]))[0]
 
         explained = False
-        if u_gpu is not None and u_orc is not None and near(q, u_gpu, u_orc):
+        if u_gpu is not None and any(near(q, u_gpu, x) for x in un[:width]):
             explained = True
         elif at_boundary(u_orc) or at_boundary(u_gpu):
             explained = True

@@ -50,7 +50,7 @@ def _both(inst, k, ef, trace_cap=4096, **opts):
     flags = opts.get("flags", 0)
     bl = opts.get("bloom_log2") or None
     r = orc.search(inst, k=k, ef=ef, stages=1, trace_cap=trace_cap, flags=flags, bloom_log2=bl,
-                   **{kk: v for kk, v in opts.items() if kk in ("entries", "ef1") and v})
+                   **{kk: v for kk, v in opts.items() if kk in ("entries", "ef1", "width") and v})
     ix.close()
     return g, r
 
@@ -611,3 +611,48 @@ def test_degree_64_parity():
     r3 = orc.search(inst, k=10, ef=64, stages=3)
     _full_checks(inst, ids, d, 10, r3["ids"])
     ix.close()
+
+
+# ---------------------------------------------------- NEXT-f3: search width w > 1 --
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+@pytest.mark.parametrize("w", [2, 4])
+def test_width_integer_fixture_bit_exact(metric, w):
+    """Search width w (oracle O6 generalisation: the w best unchecked expanded per
+    iteration, rows in key order) on exact-arithmetic fixtures: stage ① traces,
+    lists and counters identical to the oracle's; stages ②③ (host and GPU) give
+    identical ids and distances."""
+    inst = integer_instance(seed=30 + w, metric=metric, n=400)
+    for ef in (8, 32):
+        g, r = _both(inst, 5, ef, width=w)
+        ro = orc.search(inst, k=5, ef=ef, stages=1, trace_cap=4096, width=w)
+        assert np.array_equal(g["ids"], ro["ids"]) and np.array_equal(g["d"].astype(np.float64), ro["d"])
+        assert np.array_equal(g["cand_ids"], ro["cand1_ids"])
+        for q in range(inst["queries"].shape[0]):
+            ne = int(ro["trace_nexp"][q])
+            assert list(g["trace_expand"][q][:ne]) == list(ro["trace_expand"][q][:ne]) and g["trace_nexp"][q] == ne
+        assert np.array_equal(g["n_dist1"], ro["n_dist1"])
+    ix = pa.Index.from_instance(inst)
+    ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
+    for stages in (pa.PA_STAGES_FULL, pa.PA_STAGES_FULL_GPU):
+        for ef in (8, 32):
+            ids, d = ix.search(inst["queries"], k=5, ef=ef, stages=stages, width=w)
+            r = orc.search(inst, k=5, ef=ef, stages=3, width=w)
+            assert np.array_equal(ids, r["ids"]), (stages, ef)
+            assert np.array_equal(d.astype(np.float64), r["d"]), (stages, ef)
+    with pytest.raises(pa.PAError) as e:
+        ix.search(inst["queries"], k=5, ef=32, width=w, bloom_log2=12)
+    assert e.value.status == pa.PA_ENOTSUP
+    ix.close()
+
+
+@pytest.mark.parametrize("w", [2, 3])
+def test_width_config_parity(w, s1):
+    """w > 1 on float data: tie-aware stage-① parity with the oracle's width-w search."""
+    cfg = s1["cfg"]
+    ix = pa.Index.from_instance(s1)
+    g = run_gpu(ix, s1, cfg.k, cfg.ef, trace_cap=8192, width=w)
+    ix.close()
+    r = orc.search(s1, k=cfg.k, ef=cfg.ef, stages=1, trace_cap=8192, width=w)
+    rep = compare(s1, g, r, cfg.k, cfg.ef, width=w)
+    assert not rep.fail, rep.fail[:3]
+    assert rep.exact >= 0.9 * s1["queries"].shape[0]
