@@ -70,6 +70,9 @@ def lib():
         _lib.orc_brute_force.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
                                          C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int32,
                                          C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+        _lib.orc_two_hop.restype = None
+        _lib.orc_two_hop.argtypes = [C.POINTER(OrcIndex), C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                     C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.orc_recall.restype = C.c_double
         _lib.orc_recall.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                     C.c_void_p, C.c_void_p]
@@ -151,6 +154,19 @@ def search(inst: dict, queries=None, k: int = 10, ef: int = 64, stages: int = 1,
     del keep
     for i, name in enumerate(COUNTERS[:7]):
         res[name] = res["counters"][:, i]
+    return res
+
+
+def two_hop(inst: dict, e0: int, beam: int, E: int, queries=None, threads: int = 0) -> dict:
+    """O14: two-hop entry selection from the fixed entry e0 (the FES baseline of
+    P:L986-989).  → ids [m][E] int32, d [m][E] fp64 (ascending keys), n_dist [m]."""
+    ix, keep = make_index(inst)
+    Q = _c(inst["queries"] if queries is None else queries, np.float32)
+    m = Q.shape[0]
+    res = dict(ids=np.zeros((m, E), np.int32), d=np.zeros((m, E)), n_dist=np.zeros(m, np.int64))
+    lib().orc_two_hop(C.byref(ix), _p(Q), m, int(e0), int(beam), int(E), threads, _p(res["ids"]), _p(res["d"]),
+                      _p(res["n_dist"]))
+    del keep
     return res
 
 

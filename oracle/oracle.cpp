@@ -377,6 +377,55 @@ void orc_brute_force(const double* Qh, int64_t m, int32_t qstride, const float* 
     });
 }
 
+// O14: two-hop entry selection — the baseline of §6.3 "FES analysis" (P:L986-989:
+// "the first 2-hop traversal of HNSW as the baseline, both evaluated on the GPU").
+// DESIGN.md reading Q30: from the fixed entry node e0 (hop 0) every neighbour of
+// e0 is visited (hop 1); then the `beam` hop-1 nodes with the smallest keys
+// (δ', id) are expanded in key order and their unvisited neighbours visited
+// (hop 2).  Each node is visited once (exact set, e0 included).  Entries = the E
+// smallest keys over all visited nodes, e0 included, ascending; padded (−1, +inf).
+// Queries are projected as in O1 and δ' is O2 over the reduced rows, on the
+// subgraph.
+void orc_two_hop(const OrcIndex* ix, const float* Q, int64_t m, int32_t e0, int32_t beam, int32_t E,
+                 int32_t threads, int32_t* out_ids, double* out_d, int64_t* n_dist) {
+    parallel_for(m, threads, [&](int64_t qi) {
+        const int32_t D = ix->dim, dp = ix->rdim;
+        std::vector<double> qh(D, 0.0);                        // O1
+        for (int32_t j = 0; j < D; ++j) {
+            double s = 0.0;
+            for (int32_t i = 0; i < D; ++i) s += (double)Q[qi * D + i] * (double)ix->basis[(int64_t)i * D + j];
+            qh[j] = s;
+        }
+        const int64_t rs = ix->reduced_stride ? ix->reduced_stride : dp;
+        auto dprime = [&](int32_t v) { return delta(qh.data(), ix->reduced + (int64_t)v * rs, dp, ix->metric); };
+        std::unordered_set<int32_t> vis;
+        std::vector<Cand> all;                                 // every visited node with its key
+        vis.insert(e0);
+        all.push_back(Cand{dprime(e0), e0, false});
+        std::vector<Cand> hop1;
+        for (int64_t e = ix->sub_offsets[e0]; e < ix->sub_offsets[e0 + 1]; ++e) {
+            const int32_t v = ix->sub_neighbors[e];
+            if (vis.insert(v).second) hop1.push_back(Cand{dprime(v), v, false});
+        }
+        all.insert(all.end(), hop1.begin(), hop1.end());
+        std::sort(hop1.begin(), hop1.end(), key_less);
+        for (int32_t j = 0; j < beam && j < (int32_t)hop1.size(); ++j) {
+            const int32_t u = hop1[j].id;
+            for (int64_t e = ix->sub_offsets[u]; e < ix->sub_offsets[u + 1]; ++e) {
+                const int32_t v = ix->sub_neighbors[e];
+                if (vis.insert(v).second) all.push_back(Cand{dprime(v), v, false});
+            }
+        }
+        std::sort(all.begin(), all.end(), key_less);
+        if (n_dist) n_dist[qi] = (int64_t)all.size();
+        for (int32_t j = 0; j < E; ++j) {
+            const bool ok = j < (int32_t)all.size();
+            out_ids[qi * E + j] = ok ? all[j].id : -1;
+            out_d[qi * E + j] = ok ? all[j].d : std::numeric_limits<double>::infinity();
+        }
+    });
+}
+
 // O12: mean over queries of |ret_k ∩ gt_k| / k.  ret[m][rs], gt[m][gs].
 // If gt_d and ret_d are given (tie-aware variant, Q25), a returned id counts
 // when its δ ≤ δ(gt_k[k−1]) — each returned id at most once.

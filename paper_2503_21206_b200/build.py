@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import shlex
 import os
 import subprocess
 import sys
@@ -46,7 +47,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
         return LIB
     os.makedirs(OBJ, exist_ok=True)
-    extra = []          # the kernels' tuning constants are fixed in the sources
+    # the kernels' tuning constants are fixed in the sources; PA_NVCC_EXTRA
+    # (-D overrides of those constants) exists for A/B builds in a scratch copy only
+    # (scripts/ab_variant.sh), never for the shipped library
+    extra = shlex.split(os.environ.get("PA_NVCC_EXTRA", ""))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         outs = list(ex.map(lambda s: _compile(s, extra), _sources()))
     objs = [o for o, _ in outs]

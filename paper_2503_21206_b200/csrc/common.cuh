@@ -295,6 +295,9 @@ __device__ __forceinline__ float row_dist_h(const float* __restrict__ qs, const 
 // lane r's δ'.
 // PACKED32: fp32 rows use the fp32x2 FADD2/FFMA2 form (bit-identical per element).
 // Measured on C1: 6% faster in the exact-visited kernel, 4% slower in the bloom one.
+#ifndef PA_DIST_PG_MUL
+#define PA_DIST_PG_MUL 1               // × row passes whose loads are issued together (registers ↔ MLP)
+#endif
 template <int METRIC, int NVR, bool H16, int L, bool PACKED32>
 __device__ __forceinline__ float group_dists(const float* __restrict__ qs, const unsigned char* __restrict__ base,
                                              int64_t stride, int nvr, int32_t cid, int nnew, int lane) {
@@ -302,7 +305,7 @@ __device__ __forceinline__ float group_dists(const float* __restrict__ qs, const
     const int g = lane / L, j = lane % L;
     const float4* q4 = reinterpret_cast<const float4*>(qs);
     constexpr int F = NVR > 0 ? (NVR + L - 1) / L : 1;      // chunks per lane (compile-time rows)
-    constexpr int PG = F >= 4 ? 1 : (F >= 2 ? 2 : 4);       // passes whose loads are in flight together
+    constexpr int PG = (F >= 4 ? 1 : (F >= 2 ? 2 : 4)) * PA_DIST_PG_MUL;   // passes whose loads are in flight together
     float mine = 0.f;
     for (int p0 = 0; p0 * RPP < nnew; p0 += PG) {
         uint4 v[PG][F];
