@@ -195,6 +195,25 @@ pa_status pa_search_device(pa_index* ix, const float* d_queries, int64_t m, int3
 pa_status pa_search_candidates(pa_index* ix, const float* queries, int64_t m, int32_t ef,
                                const pa_search_opts* opts, int32_t* cand_ids, float* cand_dists);
 
+/* Entry selection alone (NEXT-f4, the "FES analysis" of §6.3): the
+ * E entry ids of m DEVICE query rows [m][dim], enqueued on `stream`, not
+ * synchronised, written to d_entries [m][E] (DEVICE, −1 padded).
+ *   PA_ENTRIES_FES     : projection + FES exactly as pa_search's stage ① seeds
+ *                        (a1–a4); entries in ascending (score, id).
+ *   PA_ENTRIES_TWO_HOP : projection + the two-hop baseline (oracle O14): from
+ *                        node e0, hop 1 visits N(e0), hop 2 the neighbours of the
+ *                        `beam` nearest hop-1 nodes; entries = the E smallest
+ *                        (δ', id) over every visited node, ascending.  d_entry_dists
+ *                        [m][E] (δ', +inf padded) and d_n_dist [m] (nodes visited)
+ *                        are optional (NULL).
+ * Errors: PA_EINVAL for E < 1, E > 256, beam < 0, e0 outside [0, n), null
+ * pointers, an unknown method; PA_ENOTSUP for TWO_HOP on a max_degree-64 or
+ * binary16 index.  pa_get_stats reports ms_project and ms_fes (= the selection). */
+typedef enum { PA_ENTRIES_FES = 0, PA_ENTRIES_TWO_HOP = 1 } pa_entry_method;
+pa_status pa_entries_device(pa_index* ix, const float* d_queries, int64_t m, int32_t E, int32_t method,
+                            int32_t e0, int32_t beam, int32_t* d_entries, float* d_entry_dists,
+                            int32_t* d_n_dist, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Replication across GPUs: queries are independent, so
  * every GPU holds a full replica of the device index and searches its own shard.

@@ -29,11 +29,12 @@ PA_L2, PA_IP = 0, 1
 PA_STAGES_GPU, PA_STAGES_FULL, PA_STAGES_FULL_GPU = 1, 3, 7
 PA_NO_FES, PA_NO_STAGE2, PA_NO_STAGE1, PA_NO_PIPELINE = 1, 2, 4, 8
 PA_CHECK_SIMT, PA_CHECK_WIDE_VISITED = 1, 2
+PA_ENTRIES_FES, PA_ENTRIES_TWO_HOP = 0, 1
 
 # Symbols declared in include/pilotann.h (checked by tests/test_abi.py).
 EXPORTS = ("pa_build", "pa_attach_host", "pa_search", "pa_search_device", "pa_search_candidates",
            "pa_get_stats", "pa_destroy", "pa_last_error", "pa_version",
-           "pa_replica_meta_of", "pa_build_replica", "pa_replica_buffers")
+           "pa_replica_meta_of", "pa_build_replica", "pa_replica_buffers", "pa_entries_device")
 
 
 class PAError(RuntimeError):
@@ -117,6 +118,8 @@ def lib():
         L.pa_search_device.argtypes = [vp, vp, i64, i32, i32, C.POINTER(SearchOpts), vp, vp, C.POINTER(Debug), vp]
         L.pa_search_candidates.restype = C.c_int
         L.pa_search_candidates.argtypes = [vp, vp, i64, i32, C.POINTER(SearchOpts), vp, vp]
+        L.pa_entries_device.restype = C.c_int
+        L.pa_entries_device.argtypes = [vp, vp, i64, i32, i32, i32, i32, vp, vp, vp, vp]
         L.pa_get_stats.restype = C.c_int
         L.pa_get_stats.argtypes = [vp, C.POINTER(Stats), C.c_size_t]
         L.pa_destroy.restype = None
@@ -306,6 +309,31 @@ class Index:
         _check(lib().pa_search_device(self._h, C.c_void_p(q.data_ptr()), int(q.shape[0]), k, ef, C.byref(o),
                                       C.c_void_p(out_ids.data_ptr()), C.c_void_p(out_d.data_ptr()),
                                       C.byref(debug) if debug is not None else None, C.c_void_p(stream)))
+
+    def entries_device(self, q, E, method=PA_ENTRIES_FES, e0=0, beam=0, out=None, out_d=None, n_dist=None,
+                       stream=None):
+        """pa_entries_device: the E entries of every DEVICE query row (FES or the
+        two-hop baseline, NEXT-f4).  `out` [m][E] int32 device tensor (allocated if
+        None); `out_d` [m][E] fp32 and `n_dist` [m] int32 optional (two-hop only)."""
+        _dev_rows(q, None, self.dim, np.float32, self.device, "queries")
+        m = int(q.shape[0])
+        if out is None:
+            import torch
+            out = torch.empty(m, E, dtype=torch.int32, device=q.device)
+        _dev_rows(out, m, E, np.int32, self.device, "entries")
+        if out_d is not None:
+            _dev_rows(out_d, m, E, np.float32, self.device, "entry dists")
+        if n_dist is not None:
+            _dev_rows(n_dist.view(-1, 1), m, 1, np.int32, self.device, "n_dist")
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(q.device).cuda_stream
+        _check(lib().pa_entries_device(self._h, C.c_void_p(q.data_ptr()), m, int(E), int(method), int(e0), int(beam),
+                                       C.c_void_p(out.data_ptr()),
+                                       C.c_void_p(out_d.data_ptr()) if out_d is not None else None,
+                                       C.c_void_p(n_dist.data_ptr()) if n_dist is not None else None,
+                                       C.c_void_p(stream)))
+        return out
 
     def stats(self) -> dict:
         s = Stats()

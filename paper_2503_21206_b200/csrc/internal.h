@@ -103,6 +103,18 @@ struct Refine23 {
     int32_t* counters = nullptr;        // [m][4] n_dist2, n_dist3, 0, status
 };
 int launch_refine(const DevIndex& ix, const Refine23& a, int grid_warps, cudaStream_t s);
+
+// NEXT-f4: two-hop entry selection (oracle O14), the FES baseline of P:L986-989.
+struct TwoHopArgs {
+    int64_t m = 0;
+    int32_t E = 64, beam = 32, e0 = 0;
+    const float* qp = nullptr;          // [m][rdim_pad] q'
+    int32_t* entries = nullptr;         // [m][E] ids (−1 padded), ascending keys
+    float* entry_d = nullptr;           // [m][E] δ' (optional)
+    int32_t* n_dist = nullptr;          // [m] nodes visited (optional)
+};
+int launch_two_hop(const DevIndex& ix, const TwoHopArgs& a, cudaStream_t s);
+bool two_hop_supported(const DevIndex& ix, int E);
 int refine_max_warps(const DevIndex& ix, const Refine23& a);
 
 // kernels (each returns the number of kernel launches it enqueued)

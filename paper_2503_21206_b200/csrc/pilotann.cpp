@@ -956,6 +956,65 @@ pa_status pa_search_candidates(pa_index* ix, const float* queries, int64_t m, in
     return search_host_impl(ix, queries, m, 1, r, cand_ids, cand_dists, true);
 }
 
+pa_status pa_entries_device(pa_index* ix, const float* d_queries, int64_t m, int32_t E, int32_t method,
+                            int32_t e0, int32_t beam, int32_t* d_entries, float* d_entry_dists,
+                            int32_t* d_n_dist, void* stream) {
+    g_err.clear();
+    if (!live(ix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
+    if (m < 0) return fail(PA_EINVAL, "m < 0");
+    if (E < 1 || E > 256) return fail(PA_EINVAL, "E = %d (1..256)", E);
+    if (method != PA_ENTRIES_FES && method != PA_ENTRIES_TWO_HOP) return fail(PA_EINVAL, "unknown method %d", method);
+    if (method == PA_ENTRIES_TWO_HOP) {
+        if (beam < 0) return fail(PA_EINVAL, "beam < 0");
+        if (e0 < 0 || (int64_t)e0 >= ix->dev.n) return fail(PA_EINVAL, "e0 = %d outside [0, n)", e0);
+        if (!pa::two_hop_supported(ix->dev, E))
+            return fail(PA_ENOTSUP, "two-hop entries need an ELL-32, fp32-row index");
+    }
+    if (m > 0 && (!d_queries || !d_entries)) return fail(PA_EINVAL, "null argument");
+    std::lock_guard<std::mutex> g(ix->mu);
+    CU(cudaSetDevice(ix->device));
+    if (m == 0) return PA_OK;
+    pa_status st = ensure_ws(ix, m, E, E, 1);
+    if (st != PA_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ix->done_recorded) CU(cudaStreamWaitEvent(s, ix->done_ev, 0));
+    pa::SearchArgs a;
+    a.m = m; a.k = 1; a.ef = E; a.E = E;
+    a.q = d_queries; a.qp = ix->qp; a.qres = nullptr; a.cell = ix->cell; a.entries = d_entries;
+    a.perm = ix->perm; a.qoff = ix->qoff; a.toff = ix->toff; a.fes_scores = ix->fes_scores;
+    a.work = ix->work;
+    int launches = 0;
+    CU(cudaEventRecord(ix->ev[0], s));
+    if (pa::project_tc_supported(ix->dev, false)) {
+        launches += pa::launch_project_tc(ix->dev, a, s);
+        a.cell_ready = true;
+    } else {
+        launches += pa::launch_project(ix->dev, a, s);
+    }
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(ix->ev[1], s));
+    if (method == PA_ENTRIES_FES) {
+        if (a.cell_ready && pa::fes_tc_supported(ix->dev, E)) launches += pa::launch_fes_tc(ix->dev, a, s);
+        else launches += pa::launch_fes(ix->dev, a, s);
+    } else {
+        pa::TwoHopArgs t;
+        t.m = m; t.E = E; t.beam = beam; t.e0 = e0; t.qp = ix->qp;
+        t.entries = d_entries; t.entry_d = d_entry_dists; t.n_dist = d_n_dist;
+        launches += pa::launch_two_hop(ix->dev, t, s);
+    }
+    CU(cudaGetLastError());
+    CU(cudaMemsetAsync(ix->counters, 0, sizeof(int32_t) * 4 * (size_t)m, s));   // no stage-① counters
+    for (int i = 2; i < 5; ++i) CU(cudaEventRecord(ix->ev[i], s));
+    CU(cudaEventRecord(ix->done_ev, s));
+    ix->done_recorded = true;
+    ix->events_pending = true;
+    ix->last_full_gpu = false;
+    ix->stats = pa_stats{};
+    ix->stats.queries = m;
+    ix->stats.kernel_launches = launches;
+    return PA_OK;
+}
+
 pa_status pa_replica_meta_of(const pa_index* ix, pa_replica_meta* out) {
     g_err.clear();
     if (!live(ix)) return fail(PA_ESTATE, "invalid or destroyed index handle");
