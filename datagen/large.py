@@ -575,3 +575,113 @@ def build_instance_large(cfg, device="cuda", cache: Optional[str] = None, gt_k: 
     inst["reduced"] = rot[:, :cfg.dp]                      # strided view (row stride D)
     _log(f"{cfg.name}: X̂ to host {time.time() - t:.1f}s; instance ready in {time.time() - t0:.1f}s")
     return inst
+
+
+# ----------------------------------------------------------------------------
+# C3/C4 (100M × 768): the full vectors (307 GB) fit neither one GPU nor this
+# box's 196 GB of host RAM, so only what the GPU stage reads is materialised
+# ----------------------------------------------------------------------------
+def gen_reduced(cfg, device, chunk: int = 1 << 20, sample_cap: int = 100_000):
+    """(X_r = (X·V)[:, :d'] [N][d'] fp32 on `device`, V fp64 [D][D], queries [m][D] fp32).
+
+    X is generated chunk by chunk exactly as `datagen.gen_base` would (same
+    generator stream, same chunking), twice: pass 1 accumulates the Gram matrix
+    of the same ≤100K-row uniform sample `datagen.fit_svd` draws (in chunk order),
+    pass 2 regenerates each chunk, rotates it in fp64 and keeps the first d'
+    columns, rounded once to fp32.  The full rows are never stored."""
+    import datagen as dg
+    N, D, dp = cfg.N, cfg.D, cfg.dp
+    gchunk = 1 << 21                                              # gen_base's default chunk
+    lam, RT, centres, Kc = dg._mixture_params(cfg, device)
+    sl, RTf, cf = lam.sqrt().float(), RT.float(), centres.float()
+    rng = np.random.Generator(np.random.Philox(key=cfg.seeds["base"] + 7))
+    idx = np.sort(rng.choice(N, size=min(N, sample_cap), replace=False))
+
+    def rows():
+        g = dg._gen(cfg.seeds["base"], device)
+        for s in range(0, N, gchunk):
+            e = min(N, s + gchunk)
+            lab = torch.from_numpy(dg.cluster_of_rows(s, e - s, Kc, cfg.seeds["base"])).to(device)
+            z = torch.randn(e - s, D, generator=g, device=device, dtype=torch.float32)
+            x = cf[lab] + (z * sl[None, :]) @ RTf
+            yield s, e, x / x.norm(dim=1, keepdim=True).clamp_min(1e-12)
+
+    G = torch.zeros(D, D, dtype=torch.float64, device=device)
+    for s, e, x in rows():
+        sel = idx[(idx >= s) & (idx < e)] - s
+        if sel.size:
+            S = x[torch.from_numpy(sel).to(device)].double()
+            G += S.T @ S
+    w, V = np.linalg.eigh(G.cpu().numpy())
+    V = V[:, np.argsort(-w, kind="stable")]
+    for c in range(V.shape[1]):                                   # fit_svd's sign rule
+        nz = np.flatnonzero(np.abs(V[:, c]) > 1e-12)
+        if nz.size and V[nz[0], c] < 0:
+            V[:, c] = -V[:, c]
+    V = np.ascontiguousarray(V)
+    Vd = torch.from_numpy(V[:, :dp].copy()).to(device)
+    Xr = torch.empty(N, dp, dtype=torch.float32, device=device)
+    for s, e, x in rows():
+        for a in range(s, e, chunk):
+            b = min(e, a + chunk)
+            Xr[a:b] = (x[a - s:b - s].double() @ Vd).float()
+    return Xr, V, dg.gen_queries(cfg, device)
+
+
+def build_instance_reduced(cfg, device="cuda", cache: Optional[str] = None, gt_k: int = 100) -> dict:
+    """GPU-stage instance of a 100M × 768 config (C3/C4): `reduced` (X_r), `basis`,
+    the subgraph, member flags, FES index, queries and the subgraph ground truth
+    GT_sub (reduced space).  DESIGN.md §5: with the full rows unavailable the full
+    graph (used only to sample the members) and the subgraph are built over
+    X_r; the recipe's spectrum (α = 1.6) leaves 97 % of the variance in the leading
+    128 of 768 components.  No X̂ and no full graph: stages ②③ are not runnable
+    (PA_ESTATE), the GPU stage is complete.  Cached like build_instance_large."""
+    import datagen as dg
+    t0 = time.time()
+    cdir = os.path.join(cache, cfg.name) if cache else None
+    names = ("sub_offsets", "sub_neighbors", "member_flags", "fes_centroids", "fes_cell_off", "fes_pool_ids",
+             "gt_sub_ids")
+    hit = cdir and all(os.path.exists(os.path.join(cdir, f + ".npy")) for f in names + ("done",))
+    Xr, V, Q = gen_reduced(cfg, device)
+    _log(f"{cfg.name}: reduced rows generated (two streamed passes) in {time.time() - t0:.1f}s")
+    inst = dict(cfg=cfg, N=cfg.N, D=cfg.D, dp=cfg.dp, metric=cfg.metric, basis=V.astype(np.float32), V64=V,
+                queries=Q.cpu().numpy())
+    if hit:
+        for f in names:
+            inst[f] = np.load(os.path.join(cdir, f + ".npy"))
+        _log(f"{cfg.name}: graphs + GT loaded from {cdir}")
+    else:
+        t = time.time()
+        full = build_graph(Xr, cfg.R, None, cfg.seeds["graph"])
+        _log(f"{cfg.name}: full graph (over X_r) {time.time() - t:.1f}s")
+        flags = sample_members(full, cfg.N, cfg.ratio, cfg.seeds["sample"])
+        del full
+        torch.cuda.empty_cache() if torch.cuda.is_available() else None
+        mem = torch.from_numpy(np.flatnonzero(flags)).to(Xr.device)
+        t = time.time()
+        sub = build_graph(Xr, cfg.R, mem, cfg.seeds["graph"] + 1)
+        _log(f"{cfg.name}: subgraph ({mem.numel()} members) {time.time() - t:.1f}s")
+        inst["sub_offsets"], inst["sub_neighbors"] = rows_to_csr(sub, cfg.N, ids=mem)
+        del sub
+        inst["member_flags"] = flags
+        inst["fes_centroids"], inst["fes_cell_off"], inst["fes_pool_ids"] = dg.train_fes(
+            Xr, flags, cfg.r, cfg.n_e, cfg.seeds["fes"], metric=cfg.metric)
+        t = time.time()
+        Qh = Q.double() @ torch.from_numpy(V[:, :cfg.dp].copy()).to(Q.device)
+        inst["gt_sub_ids"], _ = dg.ground_truth(Qh, Xr, gt_k, cfg.metric, ids=mem)
+        _log(f"{cfg.name}: ground truth {time.time() - t:.1f}s")
+        del mem
+        if cdir:
+            os.makedirs(cdir, exist_ok=True)
+            for f in names:
+                np.save(os.path.join(cdir, f + ".npy"), inst[f])
+            open(os.path.join(cdir, "done.npy"), "w").close()
+    t = time.time()
+    red = np.empty((cfg.N, cfg.dp), dtype=np.float32)
+    for s in range(0, cfg.N, 1 << 22):
+        red[s:s + (1 << 22)] = Xr[s:s + (1 << 22)].cpu().numpy()
+    del Xr
+    torch.cuda.empty_cache() if torch.cuda.is_available() else None
+    inst["reduced"] = red
+    _log(f"{cfg.name}: X_r to host {time.time() - t:.1f}s; instance ready in {time.time() - t0:.1f}s")
+    return inst

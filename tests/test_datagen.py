@@ -61,3 +61,31 @@ def test_shaped_ip_structure(s2):
     assert s2["metric"] == "ip"
     norms = np.linalg.norm(s2["rotated"], axis=1)
     np.testing.assert_allclose(norms, 1.0, rtol=1e-4)                          # normalised base rows
+
+
+def test_streamed_reduced_rows_match_full_generation():
+    """C3/C4's streamed generator (datagen/large.py gen_reduced: the full rows are
+    never stored) yields the same reduced rows X_r = (X·V)[:, :d'] as generating X
+    whole, fitting V (fit_svd) and rotating it; and the reduced-only instance has
+    the GPU stage's structure (members-only subgraph, FES over members, GT_sub)."""
+    import torch
+    from datagen import large
+    cfg = dg.get_config("C3", N=20_000, D=96, dp=32, m=32, n_e=4096)
+    Xr, V, Q = large.gen_reduced(cfg, "cpu")
+    X, _ = dg.gen_base(cfg, "cpu")
+    V0 = dg.fit_svd(X, cfg.seeds["base"])
+    np.testing.assert_allclose(np.abs(V[:, :cfg.dp]), np.abs(V0[:, :cfg.dp]), atol=1e-9)
+    ref = dg.rotate(X, V0)[:, :cfg.dp]
+    np.testing.assert_allclose(Xr.numpy(), ref.numpy(), rtol=1e-5, atol=1e-6)
+    assert torch.equal(Q, dg.gen_queries(cfg, "cpu"))
+    inst = large.build_instance_reduced(cfg, device="cpu", gt_k=10)
+    flags = inst["member_flags"]
+    assert abs(flags.sum() - cfg.ratio * cfg.N) <= 0.02 * cfg.N
+    _csr_ok(inst["sub_offsets"], inst["sub_neighbors"], cfg.N, cfg.R)
+    assert np.all(np.diff(inst["sub_offsets"])[flags == 0] == 0)
+    assert np.all(flags[inst["sub_neighbors"]] == 1) and np.all(flags[inst["fes_pool_ids"]] == 1)
+    assert "rotated" not in inst and inst["reduced"].shape == (cfg.N, cfg.dp)
+    Qh = orc.project(inst["queries"], inst["basis"])
+    mem = np.flatnonzero(flags)
+    ids, _ = orc.brute_force(Qh[:, :cfg.dp], inst["reduced"], 10, ids=mem)
+    assert np.array_equal(ids, inst["gt_sub_ids"][:, :10])
