@@ -133,6 +133,6 @@ def test_entries_rejects_bad_arguments():
                      (dict(E=8, method=7), pa.PA_EINVAL)):
         E = kw.pop("E")
         with pytest.raises(pa.PAError) as ei:
-            ix.entries_device(q, E, out=torch.empty(4, max(E, 1), dtype=torch.int32, device="cuda"), **kw)
+            ix.entries_device(q, E, out=torch.empty(4, E, dtype=torch.int32, device="cuda"), **kw)
         assert ei.value.status == code
     ix.close()
