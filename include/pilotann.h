@@ -42,7 +42,7 @@ extern "C" {
 
 typedef enum {
     PA_OK = 0,
-    PA_EINVAL = -1,  /* null pointer / bad size / k<1 / ef<k / rdim>dim / max_degree>64 / ef>256 / non-finite */
+    PA_EINVAL = -1,  /* null pointer / bad size / k<1 / ef<k / rdim>dim / max_degree>64 / ef1>256 / ef2,ef3>512 / non-finite */
     PA_EGRAPH = -2,  /* CSR invalid: offsets[0]!=0, non-monotone, id out of range, self-loop, duplicate,
                         degree>max_degree, edge into a non-member, non-member with edges */
     PA_EBASIS = -3,  /* basis not orthonormal: max|VᵀV − I| > 1e-4 */
@@ -108,7 +108,8 @@ typedef struct {
  * width w = 1 (Alg 1), refine_iters = 2. */
 typedef struct {
     int32_t stages;          /* pa_stages (0 ⇒ PA_STAGES_GPU)                                 */
-    int32_t ef1, ef2, ef3;   /* per-stage candidate capacities, ≤ 256                          */
+    int32_t ef1, ef2, ef3;   /* per-stage candidate capacities: ef1 ≤ 256 (stage ①'s lists),
+                                ef2, ef3 ≤ 512 (stages ②③; pass ef1 explicitly when ef > 256)    */
     int32_t entries;         /* E entries seeded into C per query (Q8)                          */
     int32_t width;           /* search width w, 1..8 (SURVEY §8.c O6 generalisation of Alg 1: the w
                                 smallest unchecked entries are expanded per iteration, rows visited in
@@ -176,7 +177,7 @@ pa_status pa_attach_host(pa_index* ix, const int64_t* full_offsets, const int32_
  * Writes out_ids/out_dists [m][k] (HOST).  PA_STAGES_GPU returns reduced-space
  * δ' (top-k of stage ①'s C); PA_STAGES_FULL returns full-space δ over X̂ and
  * requires pa_attach_host (else PA_ESTATE).  Errors: PA_EINVAL for k<1, ef<k,
- * ef>256, m<0, null pointers. */
+ * ef1>256 or ef2/ef3>512 (after defaults), m<0, null pointers. */
 pa_status pa_search(pa_index* ix, const float* queries, int64_t m, int32_t k, int32_t ef,
                     const pa_search_opts* opts, int32_t* out_ids, float* out_dists);
 

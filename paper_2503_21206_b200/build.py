@@ -32,14 +32,47 @@ def _deps_mtime():
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src, extra):
+def _include_closure(path, seen=None):
+    """Local headers `path` includes, recursively (#include "x" resolved in csrc/
+    and include/)."""
+    import re
+    seen = set() if seen is None else seen
+    try:
+        text = open(path).read()
+    except OSError:
+        return seen
+    for name in re.findall(r'^\s*#\s*include\s+"([^"]+)"', text, re.M):
+        for d in (CSRC, os.path.join(ROOT, "include")):
+            h = os.path.join(d, name)
+            if os.path.exists(h) and h not in seen:
+                seen.add(h)
+                _include_closure(h, seen)
+                break
+    return seen
+
+
+def _deps_mtime_of(src):
+    return max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in _include_closure(src)])
+
+
+def _compile(src, extra, force=False):
+    """Compile one source unless its object is newer than it and every local
+    header it includes, and was built with the same extra flags (incremental
+    rebuilds; `--force` after changing COMMON)."""
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+    stamp = obj + ".flags"
+    flags = " ".join(extra)
+    if not force and os.path.exists(obj) and os.path.exists(stamp) and open(stamp).read() == flags \
+            and os.path.getmtime(obj) >= _deps_mtime_of(src):
+        return obj, ""
     cmd = [NVCC] + GENCODE + COMMON + extra + ["-c", src, "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if os.environ.get("PA_PTXAS_V") else []
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    with open(stamp, "w") as f:
+        f.write(flags)
     return obj, r.stderr
 
 
@@ -52,7 +85,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     # (scripts/ab_variant.sh), never for the shipped library
     extra = shlex.split(os.environ.get("PA_NVCC_EXTRA", ""))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        outs = list(ex.map(lambda s: _compile(s, extra), _sources()))
+        outs = list(ex.map(lambda s: _compile(s, extra, force), _sources()))
     objs = [o for o, _ in outs]
     if verbose:
         for _, err in outs:

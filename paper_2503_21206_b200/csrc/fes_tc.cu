@@ -8,7 +8,7 @@
 //               S = Q'_tile · EV_cellᵀ on tcgen05 (kind::tf32, 3xTF32, M = 128,
 //               N = 128 pool entries per pass, accumulator in TMEM); epilogue
 //               score = ‖e‖² − 2 q'·e (L2) or −q'·e (IP) → global scratch.
-//   k_fes_select4 / k_fes_select3 (cells > 8192 entries) : one warp per query keeps the E smallest (score, id) keys
+//   k_fes_select : one warp per query keeps the E smallest (score, id) keys by a radix select
 //               (Q10: the GEMM form is used for SELECTION only; stage ①
 //               recomputes direct-form δ).  Splitting the selection out keeps
 //               32+ warps per SM on it instead of the 4 epilogue warps of a tile.
@@ -262,31 +262,28 @@ size_t fes_scores_tma_smem(int kch) {
 }
 
 
-// Selection, two passes (far fewer instructions than merging every passing key):
-//   1. every lane keeps the KP = ceil(E/32) smallest keys of its strided share in
-//      registers; a bitwise search over the high (distance) words of those 32·KP
-//      candidates gives T = the distance word of their E-th smallest — a bound ≥
-//      the true E-th smallest distance of the row;
-//   2. all keys with distance word ≤ T (the true top-E and typically a few more)
-//      are compacted into a per-warp smem buffer and bitonic-sorted once; the
-//      first E are the entries.  A row with more than kSelCap candidates (heavy
-//      ties) falls back to the threshold + rank-merge loop.
-constexpr int kSelCap = 512;
-
-__device__ __forceinline__ void warp_bitonic_smem(uint64_t* a, int n, int lane) {
-    for (int k = 2; k <= n; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = lane; i < n; i += 32) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const uint64_t x = a[i], y = a[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((x > y) == up) { a[i] = y; a[ixj] = x; }
-                }
-            }
-            __syncwarp();
-        }
-}
+// Selection (a4, the top-E of Alg 2's within-cell scores): one warp
+// per routed query, a radix select on the orderable 32-bit images of the scores.
+//   1. the row's words (ord of the GEMM-form score) are read once as float4 —
+//      into a per-warp smem stage when the largest cell fits (STAGE), otherwise
+//      re-read from L2 per pass — and the warp AND/OR give the common prefix;
+//   2. radix passes of ≤ 8 bits below that prefix: a 256-bin smem histogram of
+//      the in-range words, a warp scan finds the bin holding the E-th smallest;
+//      stop as soon as every word up to the end of that bin is ≤ kSelMax = 256
+//      words (≥ E by construction), i.e. T = the bin's last word;
+//   3. the ≤ 256 words ≤ T become (score, pool id) keys and are bitonic-sorted in
+//      registers; the first E are the entries.  All words of one value fall in
+//      one bin, so ties are resolved by the key order (δ, id) exactly as the
+//      oracle's O4.  A row whose E-th value is shared by more than ~256 words
+//      (heavy ties; the integer fixtures) takes the threshold + rank-merge loop.
+// Per query: 1 row read + ≤ 4 histogram passes over nc/32 words per lane + one
+// ≤ 256-key sort, instead of the previous two-pass bound + smem sort of up to
+// 512 keys (which dominated at E = 224, C2: 477 µs → see DESIGN §7).
+constexpr int kSelMax = 256;          // keys sorted in registers (E ≤ 256)
+constexpr int kSelWarps = 4;
+#ifndef PA_SEL_STAGE_MAX
+#define PA_SEL_STAGE_MAX 2048         // largest cell whose words are staged in smem (8 KB per warp)
+#endif
 
 // Ascending bitonic sort of n = 32·K 64-bit keys held in registers, element
 // i = a·32 + lane in t[a]: partners at distance ≥ 32 are in the same lane.
@@ -320,34 +317,25 @@ __device__ __forceinline__ void warp_bitonic_regs(uint64_t (&t)[K], int lane) {
     }
 }
 
+// per-warp smem: histogram [256] u32, key buffer [256] u64, compaction counter,
+// then (STAGE) the row's words [wcap] u32.
+__host__ __device__ constexpr size_t sel_warp_bytes(int wcap) {
+    return 256 * 4 + kSelMax * 8 + 16 + (size_t)wcap * 4;
+}
 
-// Same two-pass selection, latency-restructured (one warp per query):
-//   * the routed cell is found lane-parallel (one ballot over qoff per 32 cells),
-//   * pass 1 reads the row as float4 with NV loads in flight per lane and keeps
-//     per-lane KP smallest 32-bit distance words only (ids are not needed to bound
-//     the E-th smallest distance),
-//   * pass 2 re-reads the row (L2), counts the words ≤ T per lane, places them by a
-//     warp prefix sum and loads the pool ids of the selected entries only,
-//   * ≤ 128 candidates are sorted in registers; larger sets take the smem sort,
-//     more than kSelCap (heavy ties) the rank-merge fallback.
-// Keys and hence entries are identical to k_fes_select4's.
-#ifndef PA_SEL_MINB
-#define PA_SEL_MINB 6
-#endif
-#ifndef PA_SEL_NV
-#define PA_SEL_NV 8
-#endif
-template <int KPMAX, int SMAX, int NV>
-__global__ void __launch_bounds__(128, PA_SEL_MINB) k_fes_select3(FesParams p, int64_t m) {
+template <bool STAGE>
+__global__ void __launch_bounds__(kSelWarps * 32) k_fes_select(FesParams p, int64_t m, int wcap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // 2·ceil(E/32) words per lane: a lane rarely holds more of the row's E smallest
-    // than that, so T is close to the true E-th smallest word and ≤ 128 keys pass
-    const int E = p.E, KP = min(KPMAX, 2 * ((E + 31) / 32));
-    uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)w * kSelCap;
-    const int64_t nwarps = (int64_t)gridDim.x * 4;
-    for (int64_t pos = (int64_t)blockIdx.x * 4 + w; pos < m; pos += nwarps) {
-        int c = 0;                                        // #cells cc in [1, r) starting at or before pos
+    const int E = p.E;
+    unsigned char* base = smem_raw + (size_t)w * sel_warp_bytes(STAGE ? wcap : 0);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(base);
+    uint64_t* keys = reinterpret_cast<uint64_t*>(base + 1024);
+    int* cnt = reinterpret_cast<int*>(base + 1024 + kSelMax * 8);
+    uint32_t* words = reinterpret_cast<uint32_t*>(base + 1024 + kSelMax * 8 + 16);
+    const int64_t nwarps = (int64_t)gridDim.x * kSelWarps;
+    for (int64_t pos = (int64_t)blockIdx.x * kSelWarps + w; pos < m; pos += nwarps) {
+        int c = 0;
         for (int c0 = 1; c0 < p.r; c0 += 32) {
             const int cc = c0 + lane;
             c += __popc(__ballot_sync(kFull, cc < p.r && __ldg(p.qoff + cc) <= pos));
@@ -357,293 +345,150 @@ __global__ void __launch_bounds__(128, PA_SEL_MINB) k_fes_select3(FesParams p, i
         const int32_t* prow = p.pool_ids + pb;
         const int32_t q = __ldg(p.perm + pos);
         const int n4 = (nc + 3) >> 2;
-        // ---- pass 1: per-lane KP smallest distance words
-        uint32_t t[KPMAX];
+        // words of chunk i4 (4 consecutive entries); entries past the cell → all-ones,
+        // never selected (every selected word is ≤ T < 0xffffffff or the index is checked)
+        auto gload4 = [&](int i4) -> uint4 {
+            const float4 v = srow4[i4];
+            uint4 r;
+            r.x = ord_of(v.x);
+            r.y = i4 * 4 + 1 < nc ? ord_of(v.y) : 0xffffffffu;
+            r.z = i4 * 4 + 2 < nc ? ord_of(v.z) : 0xffffffffu;
+            r.w = i4 * 4 + 3 < nc ? ord_of(v.w) : 0xffffffffu;
+            return r;
+        };
+        auto get4 = [&](int i4) -> uint4 {
+            if constexpr (STAGE) return reinterpret_cast<const uint4*>(words)[i4];
+            else return gload4(i4);
+        };
+        // ---- 1. read the row once (8 float4 loads in flight per lane), common prefix
+        uint32_t wand = 0xffffffffu, wor = 0u;
+        for (int t0 = 0; t0 * 32 < n4; t0 += 8) {
+            uint4 v[8];
 #pragma unroll
-        for (int i = 0; i < KPMAX; ++i) t[i] = 0xffffffffu;
-        for (int i0 = 0; i0 < n4; i0 += 32 * NV) {
-            float4 v[NV];
-#pragma unroll
-            for (int u = 0; u < NV; ++u) {
-                const int i4 = i0 + u * 32 + lane;
-                v[u] = i4 < n4 ? srow4[i4] : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int u = 0; u < 8; ++u) {
+                const int i4 = (t0 + u) * 32 + lane;
+                v[u] = i4 < n4 ? gload4(i4) : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
             }
 #pragma unroll
-            for (int u = 0; u < NV; ++u) {
-                const int e0 = (i0 + u * 32 + lane) * 4;
-                const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+            for (int u = 0; u < 8; ++u) {
+                const int i4 = (t0 + u) * 32 + lane;
+                if (i4 < n4) {
+                    if constexpr (STAGE) reinterpret_cast<uint4*>(words)[i4] = v[u];
+                    const uint32_t x[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (i4 * 4 + k < nc) { wand &= x[k]; wor |= x[k]; }
+                }
+            }
+        }
+        wand = __reduce_and_sync(kFull, wand);
+        wor = __reduce_or_sync(kFull, wor);
+        // ---- 2. threshold T: count(words ≤ T) in [min(nc, E), kSelMax]
+        uint32_t T = 0xfffffffeu;                       // nc ≤ kSelMax: every entry
+        bool ties = false;
+        if (nc > kSelMax) {
+            int nbits = 32 - __clz(wand ^ wor);         // bits below the common prefix
+            uint32_t prefix = wand;                     // bits ≥ nbits are fixed
+            int below = 0;                              // words < the current range
+            if (nbits == 0) ties = true;                // every word equal (nc > 256 ties)
+            while (!ties) {
+                const int s = nbits > 8 ? nbits - 8 : 0;
+                const uint32_t dmask = (1u << (nbits - s)) - 1u;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
+                __syncwarp();
+                for (int i4 = lane; i4 < n4; i4 += 32) {
+                    const uint4 v = get4(i4);
+                    const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (i4 * 4 + k < nc && (nbits == 32 || (x[k] >> nbits) == (prefix >> nbits)))
+                            atomicAdd(&hist[(x[k] >> s) & dmask], 1u);
+                }
+                __syncwarp();
+                uint32_t h[8], sum = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { h[i] = hist[lane * 8 + i]; sum += h[i]; }
+                uint32_t incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                // the lane whose 8 bins hold the E-th smallest word
+                const unsigned hit = __ballot_sync(kFull, below + (int)(incl - sum) < E && below + (int)incl >= E);
+                const int src = __ffs(hit) - 1;
+                int bin = 0, before = 0, inbin = 0;
+                if (lane == src) {
+                    int run = below + (int)(incl - sum);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        if (run < E && run + (int)h[i] >= E && inbin == 0) { bin = lane * 8 + i; before = run; inbin = (int)h[i]; }
+                        run += (int)h[i];
+                    }
+                }
+                bin = __shfl_sync(kFull, bin, src);
+                before = __shfl_sync(kFull, before, src);
+                inbin = __shfl_sync(kFull, inbin, src);
+                const uint32_t pre = (nbits == 32 ? 0u : (prefix >> nbits) << nbits) | ((uint32_t)bin << s);
+                if (before + inbin <= kSelMax) {       // every word ≤ the bin's last word
+                    T = pre | ((1u << s) - 1u);
+                    break;
+                }
+                if (s == 0) { ties = true; break; }     // > 256 words share the E-th value
+                prefix = pre;
+                below = before;
+                nbits = s;
+                __syncwarp();
+            }
+        }
+        if (!ties) {
+            // ---- 3. compact the ≤ 256 words ≤ T as (δ, id) keys, sort, emit the first E
+            if (lane == 0) *cnt = 0;
+            __syncwarp();
+            for (int i4 = lane; i4 < n4; i4 += 32) {
+                const uint4 v = get4(i4);
+                const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    if (e0 + k >= nc) continue;
-                    uint32_t x = ord_of(f[k]);
-                    if (x < t[KP - 1]) {
-#pragma unroll
-                        for (int i = 0; i < KPMAX; ++i)
-                            if (i < KP && x < t[i]) { const uint32_t y = t[i]; t[i] = x; x = y; }
+                    const int e = i4 * 4 + k;
+                    if (e < nc && x[k] <= T) {
+                        const int at = atomicAdd(cnt, 1);
+                        keys[at] = ((uint64_t)x[k] << 32) | ((uint64_t)(uint32_t)__ldg(prow + e) << 1);
                     }
                 }
             }
-        }
-        uint32_t T = 0xffffffffu;
-        if (nc > E) {
-            uint32_t lo = 0;                              // largest T with count(< T) < E
-            for (int b = 31; b >= 0; --b) {
-                const uint32_t trial = lo | (1u << b);
-                int cnt = 0;
-#pragma unroll
-                for (int i = 0; i < KPMAX; ++i) cnt += (i < KP && t[i] < trial) ? 1 : 0;
-                cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
-                if (cnt < E) lo = trial;
-            }
-            T = lo;
-        }
-        // ---- pass 2: compact every key with distance word ≤ T
-        int M = 0;
-        bool overflow = false;
-        for (int i0 = 0; i0 < n4 && !overflow; i0 += 32 * NV) {
-            float4 v[NV];
-#pragma unroll
-            for (int u = 0; u < NV; ++u) {
-                const int i4 = i0 + u * 32 + lane;
-                v[u] = i4 < n4 ? srow4[i4] : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            uint32_t sel = 0;                             // bit u*4+k: element selected
-            int cnt = 0;
-#pragma unroll
-            for (int u = 0; u < NV; ++u) {
-                const int e0 = (i0 + u * 32 + lane) * 4;
-                const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const bool in = e0 + k < nc && ord_of(f[k]) <= T;
-                    sel |= in ? (1u << (u * 4 + k)) : 0u;
-                    cnt += in ? 1 : 0;
-                }
-            }
-            int incl = cnt;                               // warp inclusive prefix sum of the counts
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int total = __shfl_sync(kFull, incl, 31);
-            if (M + total > kSelCap) { overflow = true; break; }
-            int at = M + incl - cnt;
-#pragma unroll
-            for (int u = 0; u < NV; ++u) {
-                const int e0 = (i0 + u * 32 + lane) * 4;
-                const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (sel & (1u << (u * 4 + k))) buf[at++] = make_key(f[k], __ldg(prow + e0 + k));
-            }
-            M += total;
-        }
-        __syncwarp();
-        if (!overflow && M <= 128) {
-            uint64_t t4[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) t4[a] = a * 32 + lane < M ? buf[a * 32 + lane] : kKeyInf;
-            warp_bitonic_regs<4>(t4, lane);
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int j = a * 32 + lane;
-                if (j < E) p.entries[(int64_t)q * E + j] = j < M ? key_id(t4[a]) : -1;
-            }
-            for (int j = 128 + lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = -1;
-        } else if (!overflow) {
-            int n2 = 32;
-            while (n2 < M) n2 <<= 1;
-            for (int i = M + lane; i < n2; i += 32) buf[i] = kKeyInf;
             __syncwarp();
-            warp_bitonic_smem(buf, n2, lane);
-            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < M ? key_id(buf[j]) : -1;
-        } else {                                          // heavy ties: threshold + rank merge
-            uint64_t* C = buf;
+            const int M = *cnt;
+            auto sort_regs = [&](auto tag) {
+                constexpr int K = decltype(tag)::value;
+                uint64_t tk[K];
+#pragma unroll
+                for (int a = 0; a < K; ++a) tk[a] = a * 32 + lane < M ? keys[a * 32 + lane] : kKeyInf;
+                warp_bitonic_regs<K>(tk, lane);
+#pragma unroll
+                for (int a = 0; a < K; ++a) {
+                    const int j = a * 32 + lane;
+                    if (j < E) p.entries[(int64_t)q * E + j] = j < M ? key_id(tk[a]) : -1;
+                }
+                for (int j = 32 * K + lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = -1;
+            };
+            if (M <= 32) sort_regs(std::integral_constant<int, 1>{});
+            else if (M <= 64) sort_regs(std::integral_constant<int, 2>{});
+            else if (M <= 128) sort_regs(std::integral_constant<int, 4>{});
+            else sort_regs(std::integral_constant<int, 8>{});
+        } else {                                        // heavy ties: threshold + rank merge
+            uint64_t* C = keys;
             int csz = 0;
-            const float* srow = p.scores + pos * p.sstride;
             for (int j0 = 0; j0 < nc; j0 += 32) {
                 const int j = j0 + lane;
-                const uint64_t key = j < nc ? make_key(srow[j], __ldg(prow + j)) : kKeyInf;
+                const uint64_t key = j < nc ? make_key(p.scores[pos * p.sstride + j], __ldg(prow + j)) : kKeyInf;
                 const uint64_t thresh = csz == E ? C[E - 1] : kKeyInf;
                 const bool pass = key < thresh;
                 const unsigned pbal = __ballot_sync(kFull, pass);
                 if (pbal == 0) continue;
                 int minr;
-                csz = rank_merge<SMAX>(C, csz, E, key, pass, pbal, lane, minr);
-            }
-            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < csz ? key_id(C[j]) : -1;
-        }
-        __syncwarp();
-    }
-}
-
-// Selection with ~3× fewer instructions than k_fes_select3 (one warp per query):
-//   pass 1: lane l reads float4 chunks t·32 + l of the row (t < 16·G, all of a
-//           round's 8 loads in flight) and keeps the minimum distance word of each
-//           group of G consecutive chunks of its own → ≤ 16 group minima per lane
-//           (512 per warp, each an actual entry);
-//   T     : a bitwise search over bits 31..8 of those minima for the smallest
-//           24-bit prefix with ≥ E minima at or below it, low byte filled — at
-//           least E entries have a word ≤ T, so the E smallest keys all do;
-//   pass 2: every entry with word ≤ T is placed by a warp prefix sum as its index,
-//           keys (score, pool id) are built for the ≤ kSelCap selected only, and
-//           ≤ 128 are sorted in registers (smem sort / rank merge fallbacks).
-// With 4-entry groups ~E·1.1 entries pass (vs > 128 for per-lane top-KP lists of
-// words, which the previous selections sorted in smem).  Entries are identical.
-template <int SMAX, int G>
-__global__ void __launch_bounds__(128, 4) k_fes_select4(FesParams p, int64_t m) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int E = p.E;
-    constexpr int NT = 16 * G;                            // float4 chunks per lane (nc ≤ 2048·G)
-    uint64_t* buf = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)w * kSelCap;
-    const int64_t nwarps = (int64_t)gridDim.x * 4;
-    for (int64_t pos = (int64_t)blockIdx.x * 4 + w; pos < m; pos += nwarps) {
-        int c = 0;
-        for (int c0 = 1; c0 < p.r; c0 += 32) {
-            const int cc = c0 + lane;
-            c += __popc(__ballot_sync(kFull, cc < p.r && __ldg(p.qoff + cc) <= pos));
-        }
-        const int pb = __ldg(p.cell_off + c), nc = __ldg(p.cell_off + c + 1) - pb;
-        const float* srow = p.scores + pos * p.sstride;
-        const float4* srow4 = reinterpret_cast<const float4*>(srow);
-        const int32_t* prow = p.pool_ids + pb;
-        const int32_t q = __ldg(p.perm + pos);
-        const int n4 = (nc + 3) >> 2;
-        auto word4 = [&](const float4 v, int i4, uint32_t (&wd)[4]) {
-            const float f[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) wd[k] = (i4 * 4 + k < nc) ? ord_of(f[k]) : 0xffffffffu;
-        };
-        // ---- pass 1: group minima (fminf on the scores, ordered word of the minimum only)
-        const float kInf = __int_as_float(0x7f800000);
-        float fm[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) fm[i] = kInf;
-#pragma unroll
-        for (int t0 = 0; t0 < NT; t0 += 8) {
-            if (t0 * 32 >= n4) break;                      // warp-uniform
-            float4 v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i4 = (t0 + u) * 32 + lane;
-                v[u] = i4 < n4 ? srow4[i4] : make_float4(kInf, kInf, kInf, kInf);
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i4 = (t0 + u) * 32 + lane;
-                float4 x = v[u];
-                if (i4 * 4 + 3 >= nc) {                    // ragged tail of the cell
-                    if (i4 * 4 + 1 >= nc) x.y = kInf;
-                    if (i4 * 4 + 2 >= nc) x.z = kInf;
-                    if (i4 * 4 + 3 >= nc) x.w = kInf;
-                }
-                fm[(t0 + u) / G] = fminf(fm[(t0 + u) / G], fminf(fminf(x.x, x.y), fminf(x.z, x.w)));
-            }
-        }
-        uint32_t mn[16];                                   // ord is monotone: ord(min) = min(ord)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) mn[i] = ord_of(fm[i]);
-        uint32_t T = 0xffffffffu;
-        if (nc > E) {
-            uint32_t lo = 0;                              // largest prefix with count(< prefix) < E
-            for (int b = 31; b >= 12; --b) {
-                const uint32_t trial = lo | (1u << b);
-                int cnt = 0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) cnt += mn[i] < trial ? 1 : 0;
-                cnt = (int)__reduce_add_sync(kFull, (unsigned)cnt);
-                if (cnt < E) lo = trial;
-            }
-            T = lo | 0xfffu;                              // count(minima ≤ T) ≥ E
-        }
-        // ---- pass 2: indices of the entries with word ≤ T, by warp prefix sums
-        int M = 0;
-        bool overflow = false;
-#pragma unroll
-        for (int t0 = 0; t0 < NT; t0 += 8) {
-            if (t0 * 32 >= n4 || overflow) break;          // warp-uniform
-            float4 v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i4 = (t0 + u) * 32 + lane;
-                v[u] = i4 < n4 ? srow4[i4] : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            uint32_t sel = 0;
-            int cnt = 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i4 = (t0 + u) * 32 + lane;
-                uint32_t wd[4];
-                word4(v[u], i4, wd);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const bool in = wd[k] <= T && i4 * 4 + k < nc;
-                    sel |= in ? (1u << (u * 4 + k)) : 0u;
-                    cnt += in ? 1 : 0;
-                }
-            }
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int total = __shfl_sync(kFull, incl, 31);
-            if (M + total > kSelCap) { overflow = true; break; }
-            int at = M + incl - cnt;
-            while (sel) {                                 // this lane's selected entries (~E/32 per round)
-                const int b = __ffs(sel) - 1;
-                sel &= sel - 1;
-                buf[at++] = (uint64_t)(((t0 + (b >> 2)) * 32 + lane) * 4 + (b & 3));
-            }
-            M += total;
-        }
-        __syncwarp();
-        if (!overflow) {
-            for (int i = lane; i < M; i += 32) {          // keys of the selected entries only
-                const int e = (int)buf[i];
-                buf[i] = make_key(__ldg(srow + e), __ldg(prow + e));
-            }
-            __syncwarp();
-        }
-        auto sort_regs = [&](auto tag) {
-            constexpr int K = decltype(tag)::value;
-            uint64_t tk[K];
-#pragma unroll
-            for (int a = 0; a < K; ++a) tk[a] = a * 32 + lane < M ? buf[a * 32 + lane] : kKeyInf;
-            warp_bitonic_regs<K>(tk, lane);
-#pragma unroll
-            for (int a = 0; a < K; ++a) {
-                const int j = a * 32 + lane;
-                if (j < E) p.entries[(int64_t)q * E + j] = j < M ? key_id(tk[a]) : -1;
-            }
-            for (int j = 32 * K + lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = -1;
-        };
-        if (!overflow && M <= 128) {
-            sort_regs(std::integral_constant<int, 4>{});
-        } else if (!overflow && M <= 256) {
-            sort_regs(std::integral_constant<int, 8>{});
-        } else if (!overflow) {
-            int n2 = 32;
-            while (n2 < M) n2 <<= 1;
-            for (int i = M + lane; i < n2; i += 32) buf[i] = kKeyInf;
-            __syncwarp();
-            warp_bitonic_smem(buf, n2, lane);
-            for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < M ? key_id(buf[j]) : -1;
-        } else {                                          // heavy ties: threshold + rank merge
-            uint64_t* C = buf;
-            int csz = 0;
-            for (int j0 = 0; j0 < nc; j0 += 32) {
-                const int j = j0 + lane;
-                const uint64_t key = j < nc ? make_key(srow[j], __ldg(prow + j)) : kKeyInf;
-                const uint64_t thresh = csz == E ? C[E - 1] : kKeyInf;
-                const bool pass = key < thresh;
-                const unsigned pbal = __ballot_sync(kFull, pass);
-                if (pbal == 0) continue;
-                int minr;
-                csz = rank_merge<SMAX>(C, csz, E, key, pass, pbal, lane, minr);
+                csz = rank_merge<8>(C, csz, E, key, pass, pbal, lane, minr);
             }
             for (int j = lane; j < E; j += 32) p.entries[(int64_t)q * E + j] = j < csz ? key_id(C[j]) : -1;
         }
@@ -681,27 +526,17 @@ int launch_fes_tc(const DevIndex& ix, const SearchArgs& a, cudaStream_t s) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaLaunchKernel(fn, dim3(grid), dim3(160), args, smem, s);
     }
-    // selection: k_fes_select4 up to 8192-entry cells, k_fes_select3 above (same entries)
-    void* sel;
-    size_t ssm = (size_t)4 * kSelCap * 8;
-    if (ix.max_cell <= 2048 * 4) {
-        const int SM = a.E <= 64 ? 2 : a.E <= 128 ? 4 : 8;
-        const int G = ix.max_cell <= 2048 ? 1 : ix.max_cell <= 4096 ? 2 : 4;
-        void* t[3][3] = {{(void*)k_fes_select4<2, 1>, (void*)k_fes_select4<2, 2>, (void*)k_fes_select4<2, 4>},
-                         {(void*)k_fes_select4<4, 1>, (void*)k_fes_select4<4, 2>, (void*)k_fes_select4<4, 4>},
-                         {(void*)k_fes_select4<8, 1>, (void*)k_fes_select4<8, 2>, (void*)k_fes_select4<8, 4>}};
-        sel = t[SM == 2 ? 0 : SM == 4 ? 1 : 2][G == 1 ? 0 : G == 2 ? 1 : 2];
-    } else {
-        constexpr int NV = PA_SEL_NV;
-        sel = a.E <= 32 ? (void*)k_fes_select3<2, 2, NV> : a.E <= 64 ? (void*)k_fes_select3<4, 2, NV>
-            : a.E <= 96 ? (void*)k_fes_select3<6, 4, NV> : a.E <= 128 ? (void*)k_fes_select3<8, 4, NV>
-            : (void*)k_fes_select3<16, 8, NV>;
-    }
+    // selection: the row's words staged in smem when the largest cell fits
+    // PA_SEL_STAGE_MAX entries (occupancy vs re-reading the row from L2 per pass)
+    const bool stage = ix.max_cell <= PA_SEL_STAGE_MAX;
+    const int wcap = stage ? (ix.max_cell + 3) / 4 * 4 : 0;
+    void* sel = stage ? (void*)k_fes_select<true> : (void*)k_fes_select<false>;
+    const size_t ssm = (size_t)kSelWarps * sel_warp_bytes(wcap);
     cudaFuncSetAttribute(sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-    int64_t blocks = (a.m + 3) / 4;
     int64_t m = a.m;
-    void* args2[] = {&p, &m};
-    cudaLaunchKernel(sel, dim3((unsigned)blocks), dim3(128), args2, ssm, s);
+    int wc = wcap;
+    void* args2[] = {&p, &m, &wc};
+    cudaLaunchKernel(sel, dim3((unsigned)((a.m + kSelWarps - 1) / kSelWarps)), dim3(kSelWarps * 32), args2, ssm, s);
     return 3;
 }
 

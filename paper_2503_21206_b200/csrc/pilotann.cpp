@@ -239,7 +239,11 @@ pa_status resolve(const pa_search_opts* o, int32_t k, int32_t ef, Resolved* r, i
     r->bloom_log2 = o->bloom_log2;
     if (r->bloom_log2 != 0 && (r->bloom_log2 < 7 || r->bloom_log2 > 16))
         return fail(PA_EINVAL, "bloom_log2 = %d (0 or 7..16)", r->bloom_log2);
-    if (r->ef1 > 256 || r->ef2 > 256 || r->ef3 > 256) return fail(PA_EINVAL, "ef > 256");
+    // stage ① (and its FES entries) is bounded by the traversal kernels' 256-key lists;
+    // the refinement stages ②③ keep up to 512 (the ef stage ③ needs for full-space
+    // Recall@10 = 0.90 at 100M, DESIGN §3 reading R-ef)
+    if (r->ef1 > 256) return fail(PA_EINVAL, "ef1 = %d > 256", r->ef1);
+    if (r->ef2 > 512 || r->ef3 > 512) return fail(PA_EINVAL, "ef2/ef3 > 512");
     if (r->ef1 < 1 || r->ef2 < 1 || r->ef3 < 1 || r->E < 1 || r->E > 1024) return fail(PA_EINVAL, "bad ef/entries");
     if (r->stages == PA_STAGES_GPU && k > r->ef1) return fail(PA_EINVAL, "k = %d > ef1 = %d", k, r->ef1);
     if (r->stages != PA_STAGES_GPU && (k > r->ef3 || k > r->ef2)) return fail(PA_EINVAL, "k > ef2/ef3");

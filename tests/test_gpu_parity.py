@@ -22,13 +22,13 @@ def _built():
     g.build_library()
 
 
-def integer_instance(n=300, D=16, R=8, m=40, seed=5, r=4, metric="l2", member_ratio=0.6):
+def integer_instance(n=300, D=16, R=8, m=40, seed=5, r=4, metric="l2", member_ratio=0.6, vals=4):
     """All coordinates small integers and V a signed permutation: every fp32
     operation of the GPU path is exact, so trajectories must be bit-exact
     INCLUDING ties (many exact ties by construction)."""
     rng = np.random.default_rng(seed)
     inst = tiny_instance(n=n, D=D, dp=D // 2, R=R, m=m, seed=seed, r=r, metric=metric, member_ratio=member_ratio)
-    X = rng.integers(-4, 5, size=(n, D)).astype(np.float32)
+    X = rng.integers(-vals, vals + 1, size=(n, D)).astype(np.float32)
     perm = rng.permutation(D)
     sign = np.where(rng.random(D) < 0.5, -1.0, 1.0)
     V = np.zeros((D, D), np.float32)
@@ -36,7 +36,7 @@ def integer_instance(n=300, D=16, R=8, m=40, seed=5, r=4, metric="l2", member_ra
     Xh = (X.astype(np.float64) @ V.astype(np.float64)).astype(np.float32)
     inst["basis"], inst["rotated"] = V, Xh
     inst["reduced"] = np.ascontiguousarray(Xh[:, :D // 2])
-    inst["queries"] = rng.integers(-4, 5, size=(m, D)).astype(np.float32)
+    inst["queries"] = rng.integers(-vals, vals + 1, size=(m, D)).astype(np.float32)
     pool = inst["fes_pool_ids"]
     cuts = inst["fes_cell_off"]
     inst["fes_centroids"] = np.stack([np.round(inst["reduced"][pool[cuts[c]:cuts[c + 1]]].mean(0))
@@ -280,6 +280,26 @@ def test_fes_selection_large_cells(r):
         assert rep.exact >= 0.9 * 64
 
 
+@pytest.mark.parametrize("vals,r", [(4, 1), (4, 4), (1, 2), (1, 8)])
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_fes_selection_ties_bit_exact(vals, r, metric):
+    """FES top-E (k_fes_select's radix select) on integer inputs, where every score
+    is exact and ties are everywhere: the entries must equal the oracle's O4
+    entries element by element (order (δ, id)), E = 8 … 256.  vals = 1
+    ({−1, 0, 1} coordinates) puts hundreds of pool entries on one score, which
+    takes the heavy-tie path; cells of 3000/1500 entries take the unstaged path,
+    750/375 the smem-staged one."""
+    inst = integer_instance(n=3000, D=16, R=8, m=64, seed=60 + vals + r, r=r, metric=metric, member_ratio=1.0,
+                            vals=vals)
+    ix = pa.Index.from_instance(inst)
+    for E in (8, 100, 256):
+        g = run_gpu(ix, inst, 5, E)
+        o = orc.search(inst, k=5, ef=E, stages=1)
+        assert np.array_equal(g["cell"], o["cell"]), E
+        assert np.array_equal(g["entries"], o["entries"]), (E, np.flatnonzero((g["entries"] != o["entries"]).any(1))[:5])
+    ix.close()
+
+
 # ------------------------------------------------ NEXT-f1: bloom visited set --
 # The paper's shared-memory bloom filter (P:L392-395) vs the oracle's O13 mode on
 # the same filter definition: false positives are part of the method, so the
@@ -369,6 +389,24 @@ def test_full_gpu_integer_fixture_bit_exact(metric, flags):
         r = orc.search(inst, k=5, ef=ef, stages=3, flags=flags)
         assert np.array_equal(ids, r["ids"]), ef
         assert np.array_equal(d.astype(np.float64), r["d"]), ef
+    ix.close()
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_large_ef3_integer_fixture_bit_exact(metric):
+    """ef2/ef3 above stage ①'s 256 (up to 512; stage ① kept at ef1 = E = 200):
+    PA_STAGES_FULL (host ②③) and PA_STAGES_FULL_GPU (k_refine with 512-key lists)
+    equal the oracle's three stages id for id and distance for distance."""
+    inst = integer_instance(seed=23, metric=metric, n=2000, m=24)
+    ix = pa.Index.from_instance(inst)
+    ix.attach_host(inst["full_offsets"], inst["full_neighbors"], inst["rotated"])
+    for ef, ef2 in ((300, 0), (512, 0), (400, 450)):
+        over = dict(ef1=200, entries=200) | (dict(ef2=ef2) if ef2 else {})
+        r = orc.search(inst, k=10, ef=ef, stages=3, **over)
+        for stages in (pa.PA_STAGES_FULL, pa.PA_STAGES_FULL_GPU):
+            ids, d = ix.search(inst["queries"], k=10, ef=ef, stages=stages, **over)
+            assert np.array_equal(ids, r["ids"]), (ef, stages)
+            assert np.array_equal(d.astype(np.float64), r["d"]), (ef, stages)
     ix.close()
 
 
