@@ -2,6 +2,10 @@
 #include "traverse_kernel.cuh"
 
 namespace pa {
+namespace trav {
+void* refine_pick_m0(int cap, int D, bool compact);   // stages23_inst_m*.cu
+void* refine_pick_m1(int cap, int D, bool compact);
+}  // namespace trav
 namespace {
 using trav::kTW;
 
@@ -9,24 +13,10 @@ bool refine_compact(const DevIndex& ix, const Refine23& a) {
     return ix.n <= (1 << 24) && a.hash_log2 >= 11 && a.hash_log2 <= 13;
 }
 
-template <int METRIC, int VIS>
-void* pick_smax(int cap, int D) {
-    auto nvr = [&](auto smax) -> void* {
-        constexpr int SM = decltype(smax)::value;
-        if (D == 96) return (void*)trav::k_refine<METRIC, VIS, SM, 24>;
-        return (void*)trav::k_refine<METRIC, VIS, SM, 0>;
-    };
-    if (cap <= 64) return nvr(std::integral_constant<int, 2>{});
-    if (cap <= 96) return nvr(std::integral_constant<int, 3>{});
-    if (cap <= 128) return nvr(std::integral_constant<int, 4>{});
-    return nvr(std::integral_constant<int, 8>{});
-}
-
 void* pick(const DevIndex& ix, const Refine23& a) {
     const int cap = a.ef2 > a.ef3 ? a.ef2 : a.ef3;
     const bool cp = refine_compact(ix, a);
-    if (ix.metric == 0) return cp ? pick_smax<0, 1>(cap, a.D) : pick_smax<0, 0>(cap, a.D);
-    return cp ? pick_smax<1, 1>(cap, a.D) : pick_smax<1, 0>(cap, a.D);
+    return ix.metric == 0 ? trav::refine_pick_m0(cap, a.D, cp) : trav::refine_pick_m1(cap, a.D, cp);
 }
 
 size_t smem_bytes(const DevIndex& ix, const Refine23& a) {
