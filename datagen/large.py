@@ -522,8 +522,12 @@ def build_instance_large(cfg, device="cuda", cache: Optional[str] = None, gt_k: 
     t0 = time.time()
     cdir = os.path.join(cache, cfg.name) if cache else None
     names = ("full_offsets", "full_neighbors", "sub_offsets", "sub_neighbors", "member_flags",
-             "fes_centroids", "fes_cell_off", "fes_pool_ids", "gt_ids", "gt_sub_ids")
+             "fes_centroids", "fes_cell_off", "fes_pool_ids")
+    # ground truths depend on the query set, i.e. on m (queries are not prefix-stable
+    # across m): cached per m, next to the m-independent graphs
+    gt_names = {"gt_ids": f"gt_ids_m{cfg.m}", "gt_sub_ids": f"gt_sub_ids_m{cfg.m}"}
     hit = cdir and all(os.path.exists(os.path.join(cdir, f + ".npy")) for f in names + ("done",))
+    gt_hit = cdir and all(os.path.exists(os.path.join(cdir, f + ".npy")) for f in gt_names.values())
     Xh, labels, V, Q = gen_rotated(cfg, device)
     _log(f"{cfg.name}: vectors generated + rotated in {time.time() - t0:.1f}s")
     inst = dict(cfg=cfg, N=cfg.N, D=cfg.D, dp=cfg.dp, metric=cfg.metric, basis=V.astype(np.float32), V64=V,
@@ -532,7 +536,7 @@ def build_instance_large(cfg, device="cuda", cache: Optional[str] = None, gt_k: 
         del labels
         for f in names:
             inst[f] = np.load(os.path.join(cdir, f + ".npy"))
-        _log(f"{cfg.name}: graphs + GT loaded from {cdir} ({time.time() - t0:.1f}s)")
+        _log(f"{cfg.name}: graphs loaded from {cdir} ({time.time() - t0:.1f}s)")
     else:
         t = time.time()
         full = build_graph(Xh, cfg.R, None, cfg.seeds["graph"], labels=labels)
@@ -546,24 +550,31 @@ def build_instance_large(cfg, device="cuda", cache: Optional[str] = None, gt_k: 
         del labels
         _log(f"{cfg.name}: subgraph ({mem.numel()} members) {time.time() - t:.1f}s")
         inst["sub_offsets"], inst["sub_neighbors"] = rows_to_csr(sub, cfg.N, ids=mem)
-        del sub
+        del sub, mem
         inst["member_flags"] = flags
-        Xr = Xh[:, :cfg.dp]                                # view: deleted before X̂ is released
         inst["fes_centroids"], inst["fes_cell_off"], inst["fes_pool_ids"] = dg.train_fes(
-            Xr, flags, cfg.r, cfg.n_e, cfg.seeds["fes"], metric=cfg.metric)
-        if with_gt:
-            t = time.time()
-            Qh = Q.double() @ torch.from_numpy(V).to(Q.device)
-            inst["gt_ids"], _ = dg.ground_truth(Qh, Xh, gt_k, cfg.metric)
-            inst["gt_sub_ids"], _ = dg.ground_truth(Qh[:, :cfg.dp], Xr, gt_k, cfg.metric, ids=mem)
-            _log(f"{cfg.name}: ground truth {time.time() - t:.1f}s")
-        del mem, Xr
+            Xh[:, :cfg.dp], flags, cfg.r, cfg.n_e, cfg.seeds["fes"], metric=cfg.metric)
         if cdir:
             os.makedirs(cdir, exist_ok=True)
             for f in names:
-                if f in inst:
-                    np.save(os.path.join(cdir, f + ".npy"), inst[f])
+                np.save(os.path.join(cdir, f + ".npy"), inst[f])
             open(os.path.join(cdir, "done.npy"), "w").close()
+    if with_gt and gt_hit:
+        for k, f in gt_names.items():
+            inst[k] = np.load(os.path.join(cdir, f + ".npy"))
+        _log(f"{cfg.name}: ground truths (m = {cfg.m}) loaded from {cdir}")
+    elif with_gt:
+        t = time.time()
+        mem = torch.from_numpy(np.flatnonzero(inst["member_flags"])).to(Xh.device)
+        Qh = Q.double() @ torch.from_numpy(V).to(Q.device)
+        inst["gt_ids"], _ = dg.ground_truth(Qh, Xh, gt_k, cfg.metric)
+        inst["gt_sub_ids"], _ = dg.ground_truth(Qh[:, :cfg.dp], Xh[:, :cfg.dp], gt_k, cfg.metric, ids=mem)
+        del mem
+        _log(f"{cfg.name}: ground truth (m = {cfg.m}) {time.time() - t:.1f}s")
+        if cdir:
+            os.makedirs(cdir, exist_ok=True)
+            for k, f in gt_names.items():
+                np.save(os.path.join(cdir, f + ".npy"), inst[k])
     t = time.time()
     rot = np.empty((cfg.N, cfg.D), dtype=np.float32)
     step = 1 << 22
@@ -639,9 +650,10 @@ def build_instance_reduced(cfg, device="cuda", cache: Optional[str] = None, gt_k
     import datagen as dg
     t0 = time.time()
     cdir = os.path.join(cache, cfg.name) if cache else None
-    names = ("sub_offsets", "sub_neighbors", "member_flags", "fes_centroids", "fes_cell_off", "fes_pool_ids",
-             "gt_sub_ids")
+    names = ("sub_offsets", "sub_neighbors", "member_flags", "fes_centroids", "fes_cell_off", "fes_pool_ids")
+    gt_name = f"gt_sub_ids_m{cfg.m}"                      # per m (see build_instance_large)
     hit = cdir and all(os.path.exists(os.path.join(cdir, f + ".npy")) for f in names + ("done",))
+    gt_hit = cdir and os.path.exists(os.path.join(cdir, gt_name + ".npy"))
     Xr, V, Q = gen_reduced(cfg, device)
     _log(f"{cfg.name}: reduced rows generated (two streamed passes) in {time.time() - t0:.1f}s")
     inst = dict(cfg=cfg, N=cfg.N, D=cfg.D, dp=cfg.dp, metric=cfg.metric, basis=V.astype(np.float32), V64=V,
@@ -649,7 +661,7 @@ def build_instance_reduced(cfg, device="cuda", cache: Optional[str] = None, gt_k
     if hit:
         for f in names:
             inst[f] = np.load(os.path.join(cdir, f + ".npy"))
-        _log(f"{cfg.name}: graphs + GT loaded from {cdir}")
+        _log(f"{cfg.name}: graphs loaded from {cdir}")
     else:
         t = time.time()
         full = build_graph(Xr, cfg.R, None, cfg.seeds["graph"])
@@ -662,20 +674,28 @@ def build_instance_reduced(cfg, device="cuda", cache: Optional[str] = None, gt_k
         sub = build_graph(Xr, cfg.R, mem, cfg.seeds["graph"] + 1)
         _log(f"{cfg.name}: subgraph ({mem.numel()} members) {time.time() - t:.1f}s")
         inst["sub_offsets"], inst["sub_neighbors"] = rows_to_csr(sub, cfg.N, ids=mem)
-        del sub
+        del sub, mem
         inst["member_flags"] = flags
         inst["fes_centroids"], inst["fes_cell_off"], inst["fes_pool_ids"] = dg.train_fes(
             Xr, flags, cfg.r, cfg.n_e, cfg.seeds["fes"], metric=cfg.metric)
-        t = time.time()
-        Qh = Q.double() @ torch.from_numpy(V[:, :cfg.dp].copy()).to(Q.device)
-        inst["gt_sub_ids"], _ = dg.ground_truth(Qh, Xr, gt_k, cfg.metric, ids=mem)
-        _log(f"{cfg.name}: ground truth {time.time() - t:.1f}s")
-        del mem
         if cdir:
             os.makedirs(cdir, exist_ok=True)
             for f in names:
                 np.save(os.path.join(cdir, f + ".npy"), inst[f])
             open(os.path.join(cdir, "done.npy"), "w").close()
+    if gt_hit:
+        inst["gt_sub_ids"] = np.load(os.path.join(cdir, gt_name + ".npy"))
+        _log(f"{cfg.name}: GT_sub (m = {cfg.m}) loaded from {cdir}")
+    else:
+        t = time.time()
+        mem = torch.from_numpy(np.flatnonzero(inst["member_flags"])).to(Xr.device)
+        Qh = Q.double() @ torch.from_numpy(V[:, :cfg.dp].copy()).to(Q.device)
+        inst["gt_sub_ids"], _ = dg.ground_truth(Qh, Xr, gt_k, cfg.metric, ids=mem)
+        del mem
+        _log(f"{cfg.name}: ground truth (m = {cfg.m}) {time.time() - t:.1f}s")
+        if cdir:
+            os.makedirs(cdir, exist_ok=True)
+            np.save(os.path.join(cdir, gt_name + ".npy"), inst["gt_sub_ids"])
     t = time.time()
     red = np.empty((cfg.N, cfg.dp), dtype=np.float32)
     for s in range(0, cfg.N, 1 << 22):

@@ -26,4 +26,5 @@ objs = [os.path.join(b.OBJ, os.path.basename(s) + ".o") for s in b._sources()]
 subprocess.check_call([b.NVCC] + b.GENCODE + ["-shared", "-o", b.LIB] + objs + ["-lpthread"])
 PY
 fi
+rm -rf $DST/paper_2503_21206_b200/build $DST/profiles      # objects are linked in; keep the shipped copy small
 echo "built $DST ($FLAGS ${ONLY:+only $ONLY})"

@@ -89,3 +89,34 @@ def test_streamed_reduced_rows_match_full_generation():
     mem = np.flatnonzero(flags)
     ids, _ = orc.brute_force(Qh[:, :cfg.dp], inst["reduced"], 10, ids=mem)
     assert np.array_equal(ids, inst["gt_sub_ids"][:, :10])
+
+
+def test_large_instance_cache_is_per_query_count(tmp_path):
+    """The graph cache of the 100M tools is shared across query counts, the
+    ground truths are not: a second build with a different m (the scaling run's
+    N·10K queries after the 1-GPU run's 10K) reuses the graphs and gets the
+    ground truth of ITS queries — equal to an uncached build's."""
+    from datagen import large
+    cfg = dg.get_config("C3", N=12_000, D=64, dp=16, m=8, n_e=2048)
+    a = large.build_instance_reduced(cfg, device="cpu", cache=str(tmp_path), gt_k=10)
+    cfg2 = dg.get_config("C3", N=12_000, D=64, dp=16, m=12, n_e=2048)
+    b = large.build_instance_reduced(cfg2, device="cpu", cache=str(tmp_path), gt_k=10)
+    c = large.build_instance_reduced(cfg2, device="cpu", cache=None, gt_k=10)
+    assert a["gt_sub_ids"].shape[0] == 8 and b["gt_sub_ids"].shape[0] == 12
+    assert np.array_equal(b["gt_sub_ids"], c["gt_sub_ids"])
+    assert np.array_equal(b["sub_neighbors"], c["sub_neighbors"])
+    b2 = large.build_instance_reduced(cfg2, device="cpu", cache=str(tmp_path), gt_k=10)   # both cached now
+    assert np.array_equal(b2["gt_sub_ids"], c["gt_sub_ids"])
+
+
+def test_large_full_instance_cache_is_per_query_count(tmp_path):
+    """Same for the full-vector 100M tool (C2): graphs cached once, GT and GT_sub per m."""
+    from datagen import large
+    cfg = dg.get_config("C2", N=12_000, D=32, dp=16, m=8, n_e=2048)
+    large.build_instance_large(cfg, device="cpu", cache=str(tmp_path), gt_k=10)
+    cfg2 = dg.get_config("C2", N=12_000, D=32, dp=16, m=12, n_e=2048)
+    b = large.build_instance_large(cfg2, device="cpu", cache=str(tmp_path), gt_k=10)
+    c = large.build_instance_large(cfg2, device="cpu", cache=None, gt_k=10)
+    for key in ("gt_ids", "gt_sub_ids", "full_neighbors", "sub_neighbors"):
+        assert np.array_equal(b[key], c[key]), key
+    assert b["gt_ids"].shape[0] == 12
