@@ -1,6 +1,7 @@
 // Device helpers shared by the product kernels (NOT by the oracle).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -84,6 +85,69 @@ __device__ __forceinline__ int warp_merge(const uint64_t* A, int csz, uint64_t x
     return ns < cap ? ns : cap;
 }
 
+#ifndef PA_MERGE_BS_MIN_SMAX
+#define PA_MERGE_BS_MIN_SMAX 8         // binary-search merge from lists of > 128 keys (A/B: profiles/r2_ab_rank_merge.txt)
+#endif
+// Binary-search form of rank_merge (same positions, fewer instructions on long
+// lists): every passing lane finds its key's rank rc in C by a binary search of
+// the smem list (log2(32·SMAX) dependent loads).  Keys are unique, so entry i
+// moves right by #{j : rc_j ≤ i}; for the entries lane l owns (i = l + 32t) that
+// is #{j : t ≥ ⌈(rc_j − l)/32⌉⁺}: each broadcast (rc_j, key_j) adds one to byte
+// ⌈(rc_j − l)/32⌉⁺ of a packed histogram and one multiply by 0x0101…01 turns the
+// bytes into prefix sums (≤ 32 keys per byte: no carry).  A passing key lands at
+// rc + #{passing keys below it}.
+template <int SMAX>
+__device__ __forceinline__ int rank_merge_bs(uint64_t* C, int csz, int cap, uint64_t key, bool pass, unsigned pb,
+                                             int lane, int& minr) {
+    static_assert(SMAX <= 16, "two histogram words");
+    uint64_t c[SMAX];
+#pragma unroll
+    for (int t = 0; t < SMAX; ++t) {
+        const int i = lane + 32 * t;
+        c[t] = i < csz ? C[i] : kKeyInf;
+    }
+    constexpr int P = (32 * SMAX) >= 512 ? 512 : (32 * SMAX) >= 256 ? 256 : 128;   // ≤ 32·SMAX, 2P − 1 ≥ 32·SMAX
+    int rc = 0;
+    if (pass) {
+#pragma unroll
+        for (int step = P; step > 0; step >>= 1)
+            if (rc + step <= csz && C[rc + step - 1] < key) rc += step;
+    }
+    minr = (int)__reduce_min_sync(kFull, pass ? (unsigned)rc : 0xFFFFFFFFu);
+    const int np = __popc(pb);
+    uint64_t h0 = 0, h1 = 0;
+    int rn = 0;
+    while (pb) {
+        const int s = __ffs(pb) - 1;
+        pb &= pb - 1;
+        const int rj = __shfl_sync(kFull, rc, s);
+        const uint32_t kh = __shfl_sync(kFull, (uint32_t)(key >> 32), s);
+        const uint32_t kl = __shfl_sync(kFull, (uint32_t)key, s);
+        rn += ((((uint64_t)kh << 32) | kl) < key) ? 1 : 0;
+        const int d = rj - lane;
+        const int tj = d <= 0 ? 0 : (d + 31) >> 5;
+        if (tj < 8) h0 += 1ull << (8 * tj);
+        else if (SMAX > 8 && tj < 16) h1 += 1ull << (8 * (tj - 8));
+    }
+    const uint64_t p0 = h0 * 0x0101010101010101ull;
+    const uint64_t p1 = h1 * 0x0101010101010101ull + (p0 >> 56) * 0x0101010101010101ull;
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < SMAX; ++t) {
+        const int i = lane + 32 * t;
+        const int sh = (int)(((t < 8 ? p0 : p1) >> (8 * (t & 7))) & 0xFFu);
+        const int pos = i + sh;
+        if (i < csz && sh != 0 && pos < cap) C[pos] = c[t];
+    }
+    if (pass) {
+        const int pos = rc + rn;
+        if (pos < cap) C[pos] = key;
+    }
+    __syncwarp();
+    minr = minr < cap ? minr : cap;
+    return min(csz + np, cap);
+}
+
 // In-place rank merge of the passing lanes' keys (ballot `pb` ≠ 0) into the
 // sorted smem list C[0..csz) with capacity cap ≤ 32·SMAX; returns the new size
 // and (minr) the smallest position a new key landed at.  Every passing key is
@@ -95,6 +159,7 @@ __device__ __forceinline__ int warp_merge(const uint64_t* A, int csz, uint64_t x
 template <int SMAX>
 __device__ __forceinline__ int rank_merge(uint64_t* C, int csz, int cap, uint64_t key, bool pass, unsigned pb,
                                           int lane, int& minr) {
+    if constexpr (SMAX >= PA_MERGE_BS_MIN_SMAX && SMAX <= 16) return rank_merge_bs<SMAX>(C, csz, cap, key, pass, pb, lane, minr);
     uint64_t c[SMAX];
     int sh[SMAX];
 #pragma unroll
@@ -307,18 +372,42 @@ __device__ __forceinline__ float group_dists(const float* __restrict__ qs, const
     constexpr int F = NVR > 0 ? (NVR + L - 1) / L : 1;      // chunks per lane (compile-time rows)
     constexpr int PG = (F >= 4 ? 1 : (F >= 2 ? 2 : 4)) * PA_DIST_PG_MUL;   // passes whose loads are in flight together
     float mine = 0.f;
+#ifndef PA_DIST_PF
+#define PA_DIST_PF 0                   // L2 bulk prefetch of the rows beyond the first PG passes
+#endif
+    // Rows of later load passes: one 1-D bulk L2 prefetch per row (lane r, row r), so
+    // those passes' loads hit L2 instead of each paying a DRAM round trip.
+    if (PA_DIST_PF && NVR > 0 && lane >= PG * RPP && lane < nnew)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                     :: "l"(base + (int64_t)cid * stride), "r"(NVR * 16) : "memory");
+    // fp32 rows are loaded as float4 and binary16 rows as uint4 (no reinterpretation
+    // copies); lanes of rows past nnew issue no load and their registers are left
+    // unset: their sums stay inside their own L-lane group and are never returned
+    // (a zero-fill select cost ~45 register moves per expansion, ncu r2 source counters).
+#ifndef PA_DIST_NOZERO
+#define PA_DIST_NOZERO 0
+#endif
+    using VT = typename std::conditional<H16, uint4, float4>::type;
     for (int p0 = 0; p0 * RPP < nnew; p0 += PG) {
-        uint4 v[PG][F];
+        VT v[PG][F];
         int32_t rid[PG];
 #pragma unroll
         for (int pp = 0; pp < PG; ++pp) {
             const int rr = (p0 + pp) * RPP + g;
-            rid[pp] = __shfl_sync(kFull, cid, rr & 31);
+            rid[pp] = __shfl_sync(kFull, PA_DIST_NOZERO == 2 && rr >= nnew ? 0 : cid, PA_DIST_NOZERO == 2 && rr >= nnew ? 0 : (rr & 31));
             if (NVR > 0) {
-                const uint4* row = reinterpret_cast<const uint4*>(base + (int64_t)rid[pp] * stride);
+                const VT* row = reinterpret_cast<const VT*>(base + (int64_t)rid[pp] * stride);
+                const bool ok = PA_DIST_NOZERO == 2 || rr < nnew;   // 2: rows past nnew re-read row 0 of the batch (L1 hit)
 #pragma unroll
-                for (int k = 0; k < F; ++k)
-                    v[pp][k] = (rr < nnew && k * L + j < NVR) ? __ldg(row + k * L + j) : make_uint4(0u, 0u, 0u, 0u);
+                for (int k = 0; k < F; ++k) {
+#if PA_DIST_NOZERO == 1
+                    if (k * L + j < NVR && ok) v[pp][k] = __ldg(row + k * L + j);
+#elif PA_DIST_NOZERO == 2
+                    if (k * L + j < NVR) v[pp][k] = __ldg(row + k * L + j);
+#else
+                    v[pp][k] = (k * L + j < NVR && ok) ? __ldg(row + k * L + j) : VT{};
+#endif
+                }
             }
         }
 #pragma unroll
@@ -332,7 +421,7 @@ __device__ __forceinline__ float group_dists(const float* __restrict__ qs, const
                     const int c = k * L + j;
                     if (c >= NVR) continue;
                     if constexpr (H16) acc8(v[pp][k], q4[2 * c], q4[2 * c + 1], METRIC, a0, a1, a2, a3);
-                    else acc4<METRIC, PACKED32>(*reinterpret_cast<const float4*>(&v[pp][k]), q4[c], a0, a1, a2, a3);
+                    else acc4<METRIC, PACKED32>(v[pp][k], q4[c], a0, a1, a2, a3);
                 }
             } else if (rr < nnew) {                                // runtime row length (trace builds)
                 const uint4* row = reinterpret_cast<const uint4*>(base + (int64_t)rid[pp] * stride);

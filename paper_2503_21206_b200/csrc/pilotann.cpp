@@ -330,6 +330,17 @@ pa_status enqueue_gpu_stage(pa_index* ix, const float* d_q, int64_t m, int32_t k
     int maxw = pa::traverse_max_warps(ix->dev, a);
     if (maxw <= 0) return fail(PA_ENOTSUP, "traversal does not fit on an SM (ef=%d, hash_log2=%d)", r.ef1, r.hash_log2);
     int64_t gridw = std::min<int64_t>(maxw, ((m + 3) / 4) * 4);
+#ifndef PA_WAVE_BALANCE_PCT
+#define PA_WAVE_BALANCE_PCT 0          // balance the persistent grid's waves if that drops ≤ this % of its warps
+#endif
+    if (PA_WAVE_BALANCE_PCT > 0 && m > maxw) {
+        // per-query work is ≈ ef expansions whatever the query (n_exp ≈ ef), so the grid runs
+        // in near-discrete waves of gridw queries; a last wave of m mod gridw queries leaves
+        // most warps idle — spread m over the same number of waves with fewer warps instead
+        const int64_t waves = (m + maxw - 1) / maxw;
+        const int64_t bal = ((m + waves - 1) / waves + 3) / 4 * 4;
+        if (bal * 100 >= (int64_t)maxw * (100 - PA_WAVE_BALANCE_PCT)) gridw = bal;
+    }
     st = ensure_spill(ix, gridw);
     if (st != PA_OK) return st;
     if ((uint64_t)ix->epoch_base + (uint64_t)m + 1 >= 0xffffffffull) {
