@@ -324,7 +324,10 @@ __host__ __device__ constexpr size_t sel_warp_bytes(int wcap) {
 }
 
 template <bool STAGE>
-__global__ void __launch_bounds__(kSelWarps * 32) k_fes_select(FesParams p, int64_t m, int wcap) {
+#ifndef PA_SEL_MINB
+#define PA_SEL_MINB 1                  // min resident blocks per SM of k_fes_select (register budget)
+#endif
+__global__ void __launch_bounds__(kSelWarps * 32, PA_SEL_MINB) k_fes_select(FesParams p, int64_t m, int wcap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int E = p.E;
