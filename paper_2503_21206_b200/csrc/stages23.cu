@@ -32,10 +32,6 @@ int refine_max_warps(const DevIndex& ix, const Refine23& a) {
     void* fn = pick(ix, a);
     const size_t smem = smem_bytes(ix, a);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    // the full 228-KB carveout: the occupancy API sizes the persistent grid against it, while the
-    // driver's own choice can be smaller (C4 at ef 224 ran 53 % slower than at ef 192 for 13 % more
-    // work — as if 8 blocks of 22 KB were resident instead of 9; profiles/r2_bench_C4_batch_sweep.jsonl)
-    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     int blocks = 0, dev = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kTW * 32, smem);
     cudaGetDevice(&dev);

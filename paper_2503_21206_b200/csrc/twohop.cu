@@ -133,10 +133,6 @@ int launch_two_hop(const DevIndex& ix, const TwoHopArgs& a, cudaStream_t s) {
     const size_t per_warp = (size_t)((a.E + 1) & ~1) * 8 + (size_t)ix.qlen * 4 + 128 + ((size_t)4 << kHLog2);
     const size_t smem = per_warp * kHW;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    // the full 228-KB carveout: the occupancy API sizes the persistent grid against it, while the
-    // driver's own choice can be smaller (C4 at ef 224 ran 53 % slower than at ef 192 for 13 % more
-    // work — as if 8 blocks of 22 KB were resident instead of 9; profiles/r2_bench_C4_batch_sweep.jsonl)
-    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     int blocks = 0, dev = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kHW * 32, smem);
     cudaGetDevice(&dev);
