@@ -370,7 +370,11 @@ __device__ __forceinline__ float group_dists(const float* __restrict__ qs, const
     const int g = lane / L, j = lane % L;
     const float4* q4 = reinterpret_cast<const float4*>(qs);
     constexpr int F = NVR > 0 ? (NVR + L - 1) / L : 1;      // chunks per lane (compile-time rows)
-    constexpr int PG = (F >= 4 ? 1 : (F >= 2 ? 2 : 4)) * PA_DIST_PG_MUL;   // passes whose loads are in flight together
+    // passes whose loads are in flight together (≈ 16 float4 registers); whole-line rows (L = 8) keep 2
+#ifndef PA_WIDE_PG
+#define PA_WIDE_PG 2
+#endif
+    constexpr int PG = (L == 8 && F == 4 ? PA_WIDE_PG : (F >= 4 ? 1 : (F >= 2 ? 2 : 4))) * PA_DIST_PG_MUL;
     float mine = 0.f;
 #ifndef PA_DIST_PF
 #define PA_DIST_PF 0                   // L2 bulk prefetch of the rows beyond the first PG passes

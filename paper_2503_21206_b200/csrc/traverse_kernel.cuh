@@ -448,7 +448,11 @@ __global__ void __launch_bounds__(kTW * 32, VIS == 2 ? PA_TRAV_MINB_BLOOM : PA_T
         __syncwarp();
         const int32_t cid = lane < nnew ? scr[lane] : 0;
         __syncwarp();
-        const float d = group_dists<METRIC, DPS4, H16, H16 ? PA_GROUP_L16 : PA_GROUP_L32, VIS != 2>(
+#ifndef PA_WIDE_ROWS_MIN
+#define PA_WIDE_ROWS_MIN 0             // fp32 rows of ≥ this many float4 gathered by 8 lanes (128-B lines); 0 = off
+#endif
+        constexpr int LF = (PA_WIDE_ROWS_MIN > 0 && DPS4 >= PA_WIDE_ROWS_MIN) ? 8 : PA_GROUP_L32;
+        const float d = group_dists<METRIC, DPS4, H16, H16 ? PA_GROUP_L16 : LF, VIS != 2>(
             qs, rows, stride, nvr, cid, nnew, lane);
         return lane < nnew ? make_key(d, cid) : kKeyInf;
     };
